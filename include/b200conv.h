@@ -1,0 +1,134 @@
+/*
+ * b200conv.h — C ABI of libb200conv.so, the B200 (sm_100a) hot path of
+ * arXiv 2212.00404: direct, valid-mode, stride-1 convolution.
+ *
+ * Operation (§2.1 "The Convolution Models", Eq. 1):
+ *
+ *   O^m(x,y) = sum_{ch=1}^{C} sum_{i=0}^{K-1} sum_{j=0}^{K-1} I^ch(x+i, y+j) * F^{ch,m}(i,j),
+ *   x in [0, Wx-K+1), y in [0, Wy-K+1), m in [1, M]
+ *
+ * and its single-channel case C = 1 (Eq. 2).  With the reading Q1
+ * of DESIGN.md (filter row r pairs with the map row y) and
+ * 0-based indices this is
+ *
+ *   O[m][y][x] = sum_{ch,r,c} I[ch][y+r][x+c] * F[m][ch][r][c]
+ *
+ * i.e. cross-correlation (no kernel flip), identical to
+ * torch.nn.functional.conv2d(I[None], F)[0] on contiguous NCHW/OIHW tensors.
+ *
+ * Layouts (row-major, x fastest, no padding, no row pitch):
+ *   I : [C][Wy][Wx]                         (single-channel: [Wy][Wx])
+ *   F : [M][C][K][K], element (((m*C+ch)*K+r)*K+c)
+ *       "stored along the dimension ch first, and then along the dimension m"
+ *       (P:337-338); single-channel [M][K][K] "stored ... continuously"
+ *   O : [M][Wy-K+1][Wx-K+1], fully overwritten, never accumulated into.
+ *
+ * Ownership: every array pointer of the device entry points is a CUDA device
+ * pointer owned by the caller (the library allocates nothing and keeps no
+ * pointer after the call).  The *_host entry points take host pointers and
+ * manage their own stream-ordered device scratch.  O must not overlap I or F.
+ *
+ * Execution: asynchronous and stream-ordered on the given stream (a
+ * cudaStream_t / CUstream passed as void*; NULL = legacy default stream);
+ * no host synchronisation inside the device entry points.  Kernel faults
+ * surface at the caller's next synchronisation.  Reentrant: no mutable global
+ * state except one-time kernel attribute setup.
+ *
+ * Errors: the return value is a conv_status.  On any argument error nothing is
+ * launched and O is untouched.  Checks, in order:
+ *   CONV_E_SHAPE      any of C, Wx, Wy, K, M < 1, K > min(Wx, Wy),
+ *                     or an element count above 2^31-1
+ *   CONV_E_NULL       a null array pointer
+ *   CONV_E_ALIGN      a pointer not aligned to its element size
+ *   CONV_E_PRECISION  unknown precision
+ *   CONV_E_DEVICE     the current CUDA device is not sm_100 (or none exists)
+ *   CONV_E_LAUNCH     the launch itself failed (cudaGetLastError after launch)
+ */
+#ifndef B200CONV_H
+#define B200CONV_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define B200CONV_API __attribute__((visibility("default")))
+#else
+#define B200CONV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CONV_OK = 0,
+    CONV_E_SHAPE = 1,
+    CONV_E_NULL = 2,
+    CONV_E_ALIGN = 3,
+    CONV_E_PRECISION = 4,
+    CONV_E_DEVICE = 5,
+    CONV_E_LAUNCH = 6
+} conv_status;
+
+/* Arithmetic of the multi-channel path (north_star: "TF32 and BF16 inputs
+ * with FP32 accumulate ... alongside a strict-FP32 SIMT direct kernel").
+ *   CONV_FP32: I, F float; FP32 FFMA on CUDA cores (kernel KM-SIMT)
+ *   CONV_TF32: I, F float; tcgen05.mma kind::tf32, FP32 accumulate in TMEM
+ *              (operands enter the tensor core as TF32: the low 13 mantissa
+ *              bits are ignored by the hardware) (kernel KM-TC)
+ *   CONV_BF16: I, F __nv_bfloat16 (caller converts, RNE); tcgen05.mma
+ *              kind::f16 with BF16 inputs, FP32 accumulate (kernel KM-TC)
+ * O is always float. */
+typedef enum { CONV_FP32 = 0, CONV_TF32 = 1, CONV_BF16 = 2 } conv_precision;
+
+/* Single-channel convolution, Eq. 2, strict FP32 on CUDA cores
+ * (kernel KS), legacy default stream.  I [Wy][Wx], F [M][K][K], O [M][Ho][Wo]. */
+B200CONV_API int conv_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O);
+
+/* Multi-channel convolution, Eq. 1, strict FP32 (kernel KM-SIMT),
+ * legacy default stream.  I [C][Wy][Wx], F [M][C][K][K], O [M][Ho][Wo]. */
+B200CONV_API int conv_multi(const float *I, int C, int Wx, int Wy, const float *F, int K, int M, float *O);
+
+/* As conv_single on an explicit stream. */
+B200CONV_API int conv_single_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                   void *stream);
+
+/* As conv_multi with an explicit precision (conv_precision) and stream.
+ * For CONV_BF16, I and F point to bfloat16 arrays of the same shapes. */
+B200CONV_API int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                  int precision, void *stream);
+
+/* End-to-end entry points on HOST buffers (pageable or pinned): copy I and F
+ * host->device, run the same kernels as the *_ex calls, copy O device->host,
+ * and synchronise the stream before returning.  Device scratch is allocated
+ * and freed stream-ordered (cudaMallocAsync) inside the call.  For CONV_BF16
+ * the host I and F are bfloat16 arrays. */
+B200CONV_API int conv_single_host(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                     void *stream);
+B200CONV_API int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                    int precision, void *stream);
+
+/* Launch plan the device entry points use for a shape (pure function; no
+ * device access).  Every call of the hot path is exactly ONE kernel launch. */
+typedef struct {
+    int kernel;        /* 0 = KS (single FP32), 1 = KM-SIMT (multi FP32), 2 = KM-TC (tf32/bf16) */
+    int grid_x, grid_y, grid_z;
+    int block_x;
+    int cluster_x;     /* split-K factor over channels / K-blocks (1 = none) */
+    int tile_m;        /* filters per CTA tile */
+    int tile_n;        /* (wide) output pixels per CTA tile */
+    int smem_bytes;    /* dynamic shared memory per CTA */
+    int tma_f;         /* 1 if F tiles are loaded by TMA (tensor map) */
+} conv_plan;
+
+B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);
+B200CONV_API int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
+
+B200CONV_API const char *conv_status_string(int status);
+
+/* ABI version: (major << 16) | minor. */
+B200CONV_API int conv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200CONV_H */

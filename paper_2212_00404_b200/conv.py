@@ -1,0 +1,202 @@
+"""Thin Python binding of libb200conv.so (include/b200conv.h).
+
+Argument marshalling only: every step of the convolution runs in the CUDA
+kernels behind the C ABI.  PyTorch provides device memory and streams.  There
+is no CPU or eager fallback: if the library is missing or the device is not a
+B200 the calls raise.
+
+Names follow the ABI: ``conv_single``, ``conv_multi``, ``conv_single_ex``,
+``conv_multi_ex``, ``conv_single_host``, ``conv_multi_host``, plus the
+allocating conveniences ``single(I, F)`` and ``multi(I, F, precision)``, which
+consume and produce exactly the tensors ``torch.nn.functional.conv2d(I[None],
+F)[0]`` does (NCHW/OIHW, N = 1, valid, stride 1 — PAPER.md Eq. 1).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libb200conv.so")
+
+CONV_FP32, CONV_TF32, CONV_BF16 = 0, 1, 2
+PRECISIONS = {"fp32": CONV_FP32, "tf32": CONV_TF32, "bf16": CONV_BF16}
+STATUS = {0: "CONV_OK", 1: "CONV_E_SHAPE", 2: "CONV_E_NULL", 3: "CONV_E_ALIGN",
+          4: "CONV_E_PRECISION", 5: "CONV_E_DEVICE", 6: "CONV_E_LAUNCH"}
+EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv_single_host",
+           "conv_multi_host", "conv_plan_single", "conv_plan_multi", "conv_status_string",
+           "conv_version"]
+
+
+class ConvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ConvPlan(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in
+                ("kernel", "grid_x", "grid_y", "grid_z", "block_x", "cluster_x", "tile_m",
+                 "tile_n", "smem_bytes", "tma_f")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the C-ABI library (raises if it was not built — no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(f"{path} missing: build it with `python -m paper_2212_00404_b200.build`"
+                                   " (no CPU fallback exists)")
+            lib = ctypes.CDLL(path)
+            P, I32 = ctypes.c_void_p, ctypes.c_int
+            lib.conv_single.argtypes = [P, I32, I32, P, I32, I32, P]
+            lib.conv_multi.argtypes = [P, I32, I32, I32, P, I32, I32, P]
+            lib.conv_single_ex.argtypes = [P, I32, I32, P, I32, I32, P, P]
+            lib.conv_multi_ex.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
+            lib.conv_single_host.argtypes = [P, I32, I32, P, I32, I32, P, P]
+            lib.conv_multi_host.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
+            lib.conv_plan_single.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
+            lib.conv_plan_multi.argtypes = [I32, I32, I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
+            lib.conv_status_string.argtypes = [I32]
+            lib.conv_status_string.restype = ctypes.c_char_p
+            lib.conv_version.argtypes = []
+            for n in EXPORTS:
+                if n != "conv_status_string":
+                    getattr(lib, n).restype = I32
+            _lib = lib
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise ConvError(status, load().conv_status_string(status).decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _prec(p) -> int:
+    return PRECISIONS[p] if isinstance(p, str) else int(p)
+
+
+# ---------------------------------------------------------------- raw ABI names
+def conv_single(I, Wx, Wy, F, K, M, O):
+    _check(load().conv_single(_ptr(I), Wx, Wy, _ptr(F), K, M, _ptr(O)))
+
+
+def conv_multi(I, C, Wx, Wy, F, K, M, O):
+    _check(load().conv_multi(_ptr(I), C, Wx, Wy, _ptr(F), K, M, _ptr(O)))
+
+
+def conv_single_ex(I, Wx, Wy, F, K, M, O, stream=None):
+    _check(load().conv_single_ex(_ptr(I), Wx, Wy, _ptr(F), K, M, _ptr(O), _stream(stream)))
+
+
+def conv_multi_ex(I, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):
+    _check(load().conv_multi_ex(_ptr(I), C, Wx, Wy, _ptr(F), K, M, _ptr(O), _prec(precision),
+                                _stream(stream)))
+
+
+def conv_single_host(I, Wx, Wy, F, K, M, O, stream=None):
+    _check(load().conv_single_host(_ptr(I), Wx, Wy, _ptr(F), K, M, _ptr(O), _stream(stream)))
+
+
+def conv_multi_host(I, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):
+    _check(load().conv_multi_host(_ptr(I), C, Wx, Wy, _ptr(F), K, M, _ptr(O), _prec(precision),
+                                  _stream(stream)))
+
+
+def plan_single(Wx, Wy, K, M) -> dict:
+    p = ConvPlan()
+    _check(load().conv_plan_single(Wx, Wy, K, M, ctypes.byref(p)))
+    return p.as_dict()
+
+
+def plan_multi(C, Wx, Wy, K, M, precision="fp32") -> dict:
+    p = ConvPlan()
+    _check(load().conv_plan_multi(C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
+    return p.as_dict()
+
+
+def version() -> int:
+    return load().conv_version()
+
+
+# ---------------------------------------------------------------- conveniences
+def _require_cuda(*ts):
+    for t in ts:
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("expected contiguous CUDA tensors")
+
+
+def single(I: torch.Tensor, F: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """Eq. 2: I[Wy][Wx] f32, F[M][K][K] f32 -> O[M][Ho][Wo] f32 (kernel KS)."""
+    _require_cuda(I, F)
+    Wy, Wx = I.shape
+    M, K, _ = F.shape
+    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), device=I.device,
+                                                dtype=torch.float32)
+    conv_single_ex(I, Wx, Wy, F, K, M, O, stream)
+    return O
+
+
+def multi(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor | None = None,
+          stream=None):
+    """Eq. 1: I[C][Wy][Wx], F[M][C][K][K] -> O[M][Ho][Wo] f32.
+
+    precision "fp32" (KM-SIMT), "tf32" (KM-TC) take float32 I, F; "bf16"
+    (KM-TC) takes bfloat16 I, F."""
+    _require_cuda(I, F)
+    want = torch.bfloat16 if _prec(precision) == CONV_BF16 else torch.float32
+    if I.dtype != want or F.dtype != want:
+        raise ValueError(f"precision {precision} expects {want} inputs")
+    C, Wy, Wx = I.shape
+    M, C2, K, _ = F.shape
+    if C2 != C:
+        raise ValueError("channel mismatch")
+    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), device=I.device,
+                                                dtype=torch.float32)
+    conv_multi_ex(I, C, Wx, Wy, F, K, M, O, precision, stream)
+    return O
+
+
+def multi_host(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor | None = None,
+               stream=None):
+    """End-to-end on host tensors through conv_multi_host (H2D, kernel, D2H, sync)."""
+    C, Wy, Wx = I.shape
+    M, _, K, _ = F.shape
+    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), dtype=torch.float32)
+    conv_multi_host(I, C, Wx, Wy, F, K, M, O, precision, stream)
+    return O
+
+
+def single_host(I: torch.Tensor, F: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    Wy, Wx = I.shape
+    M, K, _ = F.shape
+    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), dtype=torch.float32)
+    conv_single_host(I, Wx, Wy, F, K, M, O, stream)
+    return O

@@ -1,0 +1,196 @@
+// abi.cu — the C ABI declared in include/b200conv.h: argument validation,
+// device check, dispatch to one kernel launch per call, host-buffer entry
+// points.  Every compute step of the hot path runs in the kernels; this file
+// only checks and launches.
+#include <climits>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "kernels.h"
+
+using namespace b200;
+
+namespace {
+
+int check_shape(int C, int Wx, int Wy, int K, int M) {
+    if (C < 1 || Wx < 1 || Wy < 1 || K < 1 || M < 1) return CONV_E_SHAPE;
+    if (K > Wx || K > Wy) return CONV_E_SHAPE;
+    const int64_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    if ((int64_t)C * Wx * Wy > INT_MAX) return CONV_E_SHAPE;
+    if ((int64_t)M * C * K * K > INT_MAX) return CONV_E_SHAPE;
+    if ((int64_t)M * Ho * Wo > INT_MAX) return CONV_E_SHAPE;
+    return CONV_OK;
+}
+
+bool aligned(const void *p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int check_ptrs(const void *I, const void *F, const void *O, int in_elem) {
+    if (!I || !F || !O) return CONV_E_NULL;
+    if (!aligned(I, in_elem) || !aligned(F, in_elem) || !aligned(O, 4)) return CONV_E_ALIGN;
+    return CONV_OK;
+}
+
+int check_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return CONV_E_DEVICE; }
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return CONV_E_DEVICE;
+    }
+    return (major == 10 && minor == 0) ? CONV_OK : CONV_E_DEVICE;
+}
+
+int launch_status(cudaError_t e) {
+    if (e == cudaSuccess) return CONV_OK;
+    cudaGetLastError();
+    return CONV_E_LAUNCH;
+}
+
+int run_multi(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+              int precision, cudaStream_t s) {
+    switch (precision) {
+        case CONV_FP32:
+            return launch_status(launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy,
+                                                   static_cast<const float *>(F), K, M, O, s));
+        case CONV_TF32:
+            return launch_status(launch_multi_tc(I, C, Wx, Wy, F, K, M, O, false, s));
+        case CONV_BF16:
+            return launch_status(launch_multi_tc(I, C, Wx, Wy, F, K, M, O, true, s));
+        default:
+            return CONV_E_PRECISION;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int conv_single_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                   void *stream) {
+    int st = check_shape(1, Wx, Wy, K, M);
+    if (st) return st;
+    if ((st = check_ptrs(I, F, O, 4))) return st;
+    if ((st = check_device())) return st;
+    return launch_status(launch_single(I, Wx, Wy, F, K, M, O, static_cast<cudaStream_t>(stream)));
+}
+
+int conv_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O) {
+    return conv_single_ex(I, Wx, Wy, F, K, M, O, nullptr);
+}
+
+int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                  int precision, void *stream) {
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    if ((st = check_ptrs(I, F, O, precision == CONV_BF16 ? 2 : 4))) return st;
+    if ((st = check_device())) return st;
+    return run_multi(I, C, Wx, Wy, F, K, M, O, precision, static_cast<cudaStream_t>(stream));
+}
+
+int conv_multi(const float *I, int C, int Wx, int Wy, const float *F, int K, int M, float *O) {
+    return conv_multi_ex(I, C, Wx, Wy, F, K, M, O, CONV_FP32, nullptr);
+}
+
+// ------------------------------------------------------------ host buffers
+static int host_roundtrip(const void *Ih, size_t i_bytes, const void *Fh, size_t f_bytes, float *Oh,
+                          size_t o_bytes, cudaStream_t s,
+                          int (*body)(const void *, const void *, float *, void *), void *ctx) {
+    void *Id = nullptr, *Fd = nullptr, *Od = nullptr;
+    if (cudaMallocAsync(&Id, i_bytes, s) != cudaSuccess || cudaMallocAsync(&Fd, f_bytes, s) != cudaSuccess ||
+        cudaMallocAsync(&Od, o_bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        if (Id) cudaFreeAsync(Id, s);
+        if (Fd) cudaFreeAsync(Fd, s);
+        return CONV_E_LAUNCH;
+    }
+    int st = CONV_OK;
+    if (cudaMemcpyAsync(Id, Ih, i_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(Fd, Fh, f_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        st = CONV_E_LAUNCH;
+    if (st == CONV_OK) st = body(Id, Fd, static_cast<float *>(Od), ctx);
+    if (st == CONV_OK && cudaMemcpyAsync(Oh, Od, o_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        st = CONV_E_LAUNCH;
+    cudaFreeAsync(Id, s);
+    cudaFreeAsync(Fd, s);
+    cudaFreeAsync(Od, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == CONV_OK) st = CONV_E_LAUNCH;
+    cudaGetLastError();
+    return st;
+}
+
+struct MultiCtx { int C, Wx, Wy, K, M, precision; cudaStream_t s; };
+static int multi_body(const void *I, const void *F, float *O, void *c) {
+    MultiCtx *m = static_cast<MultiCtx *>(c);
+    return run_multi(I, m->C, m->Wx, m->Wy, F, m->K, m->M, O, m->precision, m->s);
+}
+static int single_body(const void *I, const void *F, float *O, void *c) {
+    MultiCtx *m = static_cast<MultiCtx *>(c);
+    return launch_status(launch_single(static_cast<const float *>(I), m->Wx, m->Wy,
+                                       static_cast<const float *>(F), m->K, m->M, O, m->s));
+}
+
+int conv_single_host(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                     void *stream) {
+    int st = check_shape(1, Wx, Wy, K, M);
+    if (st) return st;
+    if ((st = check_ptrs(I, F, O, 4))) return st;
+    if ((st = check_device())) return st;
+    MultiCtx ctx{1, Wx, Wy, K, M, CONV_FP32, static_cast<cudaStream_t>(stream)};
+    const size_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    return host_roundtrip(I, (size_t)Wx * Wy * 4, F, (size_t)M * K * K * 4, O, (size_t)M * Ho * Wo * 4,
+                          ctx.s, single_body, &ctx);
+}
+
+int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                    int precision, void *stream) {
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    const int e = precision == CONV_BF16 ? 2 : 4;
+    if ((st = check_ptrs(I, F, O, e))) return st;
+    if ((st = check_device())) return st;
+    MultiCtx ctx{C, Wx, Wy, K, M, precision, static_cast<cudaStream_t>(stream)};
+    const size_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    return host_roundtrip(I, (size_t)C * Wx * Wy * e, F, (size_t)M * C * K * K * e, O,
+                          (size_t)M * Ho * Wo * 4, ctx.s, multi_body, &ctx);
+}
+
+// ------------------------------------------------------------ plans / misc
+int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out) {
+    int st = check_shape(1, Wx, Wy, K, M);
+    if (st) return st;
+    if (!out) return CONV_E_NULL;
+    plan_single(Wx, Wy, K, M, out);
+    return CONV_OK;
+}
+
+int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out) {
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    if (!out) return CONV_E_NULL;
+    switch (precision) {
+        case CONV_FP32: plan_multi_simt(C, Wx, Wy, K, M, out); return CONV_OK;
+        case CONV_TF32: plan_multi_tc(C, Wx, Wy, K, M, false, nullptr, out); return CONV_OK;
+        case CONV_BF16: plan_multi_tc(C, Wx, Wy, K, M, true, nullptr, out); return CONV_OK;
+        default: return CONV_E_PRECISION;
+    }
+}
+
+const char *conv_status_string(int status) {
+    switch (status) {
+        case CONV_OK: return "ok";
+        case CONV_E_SHAPE: return "shape error: a dimension < 1, K > min(Wx, Wy), or size overflow";
+        case CONV_E_NULL: return "null pointer";
+        case CONV_E_ALIGN: return "pointer not aligned to its element size";
+        case CONV_E_PRECISION: return "unknown precision";
+        case CONV_E_DEVICE: return "current CUDA device is not sm_100 (B200) or no device";
+        case CONV_E_LAUNCH: return "kernel launch or CUDA runtime error";
+        default: return "unknown status";
+    }
+}
+
+int conv_version(void) { return (1 << 16) | 0; }
+
+}  // extern "C"

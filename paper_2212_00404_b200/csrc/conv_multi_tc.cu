@@ -1,0 +1,413 @@
+// conv_multi_tc.cu — kernel KM-TC: multi-channel direct convolution (PAPER.md
+// §2.1 Eq. 1) as an implicit GEMM on the 5th-generation tensor cores
+// (tcgen05.mma, accumulators in TMEM), TF32 or BF16 inputs, FP32 accumulate.
+//
+//   D[p][m] = sum_k A[p][k] * B[m][k],   k = (ch, r, c) = ch*K*K + r*K + c
+//   A[p][k] = I[ch][p + r*Wx + c]        (im2col of I, built on chip)
+//   B[m][k] = F[m][ch][r][c] = F[m*Ktot + k]  (F as stored, row-major [M][Ktot])
+//   O[m][y][x] = D[y*Wx + x][m]          for x < Wo ("wide" pixel p = y*Wx + x)
+//
+// The reduction order k = (ch, r, c) is exactly the filter layout of the paper
+// ("along the dimension ch first"), so B is F itself: a TMA tensor
+// map loads [BN filters] x [128 B of k] boxes with the 128-B swizzle straight
+// into the canonical K-major UMMA layout (the paper's stride-fixed segment S,
+// P:603-612, becomes one 128-B TMA row).  A is gathered by four warps from the
+// L2-resident input into the same swizzled layout (one pixel row per thread,
+// 32-lane coalesced loads), fenced into the async proxy, and handed to the MMA
+// through an mbarrier ring.  Pixels go on the 128-lane M side so the epilogue
+// (tcgen05.ld -> registers -> st.global) writes 32 consecutive pixels per warp
+// instruction, coalesced.  Small layers split the k loop over a thread-block
+// cluster and reduce the partial tiles through DSMEM in fixed rank order.
+//
+// Warp roles (192 threads):
+//   warp 0      TMA producer of B (F tiles)            [elected lane]
+//   warp 1      TMEM allocator + MMA issuer            [elected lane]
+//   warps 2..5  im2col gather of A, then epilogue      [128 threads]
+#include <cstdint>
+#include <cstring>
+#include <type_traits>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace b200 {
+
+constexpr int kTcThreads = 192;
+constexpr int kTcBM = 128;            // pixels per tile (UMMA M)
+constexpr int kTcStages = 4;
+constexpr int kTcMaxSplit = 8;
+
+template <bool kTF32>
+struct TcTraits {
+    using T = typename std::conditional<kTF32, float, __nv_bfloat16>::type;
+    static constexpr int kElem = kTF32 ? 4 : 2;
+    static constexpr int kBK = 128 / kElem;           // k per stage (one 128-B swizzle row)
+    static constexpr int kUmmaK = 32 / kElem;         // k per tcgen05.mma (32 B)
+    static constexpr uint32_t kFmt = kTF32 ? 2u : 1u; // instr-desc a/b format
+};
+
+__host__ __device__ constexpr int tc_stage_bytes(int BN) { return kTcBM * 128 + BN * 128; }
+__host__ __device__ constexpr int tc_smem_bytes(int BN) {
+    return 1024 /*align slack*/ + kTcStages * tc_stage_bytes(BN) + 256 /*barriers*/;
+}
+
+// Byte offset of 16-B chunk j of row g in a K-major SWIZZLE_128B tile.
+__device__ __forceinline__ uint32_t sw128_off(int g, int j) {
+    return (uint32_t)((g >> 3) * 1024 + (g & 7) * 128 + ((j ^ (g & 7)) << 4));
+}
+
+template <bool kTF32, int BN, bool kTmaB>
+__global__ void __launch_bounds__(kTcThreads, 1)
+kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ Iv,
+            const void *__restrict__ Fv, int C, int Wx, int Wy, int K, int M,
+            float *__restrict__ O, int kb_per_split) {
+    using Tr = TcTraits<kTF32>;
+    using T = typename Tr::T;
+    constexpr int BK = Tr::kBK;
+    constexpr int STAGE = tc_stage_bytes(BN);
+    constexpr int A_BYTES = kTcBM * 128;
+    constexpr uint32_t IDESC = umma_idesc(Tr::kFmt, kTcBM, BN);
+
+    const T *__restrict__ I = static_cast<const T *>(Iv);
+    const T *__restrict__ F = static_cast<const T *>(Fv);
+    const int KK = K * K;
+    const int Ktot = C * KK;
+    const int HW = Wx * Wy;
+    const int64_t CHW = (int64_t)C * HW;
+    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int nkb = (Ktot + BK - 1) / BK;
+
+    const int S = gridDim.x;
+    const int split = blockIdx.x;
+    const int p0 = blockIdx.y * kTcBM;
+    const int n0 = blockIdx.z * BN;
+    const int kb0 = split * kb_per_split;
+    const int kb1 = min(nkb, kb0 + kb_per_split);
+    const int niter = kb1 > kb0 ? kb1 - kb0 : 0;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTcStages * STAGE);
+    uint64_t *empty = full + kTcStages;
+    uint64_t *tmem_full = empty + kTcStages;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], kTmaB ? 5 : 4);       // 4 gather warps (+1 TMA arrive.expect_tx)
+            mbar_init(&empty[s], 1);                  // tcgen05.commit
+        }
+        mbar_init(tmem_full, 1);
+        fence_mbar_init();
+        if (kTmaB) tma_prefetch_desc(&tmapF);
+    }
+    if (warp == 1) tmem_alloc<BN>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (B = F)
+        if (kTmaB && lane == 0) {
+            for (int i = 0; i < niter; ++i) {
+                const int s = i % kTcStages;
+                mbar_wait(&empty[s], ((i / kTcStages) & 1) ^ 1);
+                uint8_t *b_s = smem + s * STAGE + A_BYTES;
+                mbar_arrive_expect_tx(&full[s], BN * 128);
+                tma_load_2d(b_s, &tmapF, &full[s], (kb0 + i) * BK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            for (int i = 0; i < niter; ++i) {
+                const int s = i % kTcStages;
+                mbar_wait(&full[s], (i / kTcStages) & 1);
+                tc_fence_after();
+                const uint32_t a_addr = smem_u32(smem + s * STAGE);
+                const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / Tr::kUmmaK; ++kk) {
+                    umma_ss<kTF32>(tmem, umma_desc_k_sw128(a_addr + kk * 32),
+                                   umma_desc_k_sw128(b_addr + kk * 32), IDESC,
+                                   (i > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&empty[s]);
+            }
+            umma_commit(tmem_full);       // fires when all MMAs above are complete
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ im2col gather of A
+        const int g = threadIdx.x - 64;                  // pixel row in the tile, 0..127
+        const int p = p0 + g;
+        const bool prow = p < Ho * Wx;
+        for (int i = 0; i < niter; ++i) {
+            const int s = i % kTcStages;
+            mbar_wait(&empty[s], ((i / kTcStages) & 1) ^ 1);
+            uint8_t *a_s = smem + s * STAGE;
+            const int k0 = (kb0 + i) * BK;
+            // each lane decodes the input offset of (BK/32) k values
+            int koff[BK / 32];
+#pragma unroll
+            for (int h = 0; h < BK / 32; ++h) {
+                const int k = k0 + h * 32 + (int)lane;
+                const int ch = k / KK, rem = k - ch * KK, r = rem / K, c = rem - r * K;
+                koff[h] = k < Ktot ? ch * HW + r * Wx + c : -1;
+            }
+            if constexpr (kTF32) {
+                uint32_t v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int off = __shfl_sync(0xffffffffu, koff[0], j);
+                    const int64_t a = (int64_t)p + off;
+                    v[j] = (prow && off >= 0 && a < CHW)
+                               ? __float_as_uint(__ldg(reinterpret_cast<const float *>(I) + a))
+                               : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<uint4 *>(a_s + sw128_off(g, q)) =
+                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+                const unsigned short *Ib = reinterpret_cast<const unsigned short *>(I);
+                uint32_t v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    uint32_t lohi[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int kl = 2 * j + e;                       // 0..63
+                        const int off = __shfl_sync(0xffffffffu, koff[kl >> 5], kl & 31);
+                        const int64_t a = (int64_t)p + off;
+                        lohi[e] = (prow && off >= 0 && a < CHW) ? (uint32_t)__ldg(Ib + a) : 0u;
+                    }
+                    v[j] = lohi[0] | (lohi[1] << 16);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<uint4 *>(a_s + sw128_off(g, q)) =
+                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+            if constexpr (!kTmaB) {
+                // B rows (filters) gathered too when F rows are not 16-B aligned
+                uint8_t *b_s = a_s + A_BYTES;
+                for (int nr = g; nr < BN; nr += 128) {
+                    const int m = n0 + nr;
+                    uint32_t v[32];
+                    if constexpr (kTF32) {
+                        const float *Fm = reinterpret_cast<const float *>(F) + (int64_t)m * Ktot;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int k = k0 + j;
+                            v[j] = (m < M && k < Ktot) ? __float_as_uint(__ldg(Fm + k)) : 0u;
+                        }
+                    } else {
+                        const unsigned short *Fm =
+                            reinterpret_cast<const unsigned short *>(F) + (int64_t)m * Ktot;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int k = k0 + 2 * j;
+                            const uint32_t lo = (m < M && k < Ktot) ? (uint32_t)__ldg(Fm + k) : 0u;
+                            const uint32_t hi = (m < M && k + 1 < Ktot) ? (uint32_t)__ldg(Fm + k + 1) : 0u;
+                            v[j] = lo | (hi << 16);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4 *>(b_s + sw128_off(nr, q)) =
+                            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                }
+            }
+            fence_proxy_async_smem();        // generic-proxy stores -> visible to tcgen05
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        }
+
+        // ------------------------------------------------ epilogue
+        const int q = (int)(warp & 3);                   // TMEM lane quarter of this warp
+        const int row = q * 32 + (int)lane;              // pixel row == TMEM lane
+        const int pe = p0 + row;
+        const int y = pe / Wx, x = pe - y * Wx;
+        const bool valid = (pe < Ho * Wx) && (x < Wo);
+        const int64_t obase = (int64_t)y * Wo + x;
+        const int64_t plane = (int64_t)Ho * Wo;
+        float *P = reinterpret_cast<float *>(smem);      // [BN][128] partial tile (split > 1)
+        if (niter > 0) {
+            mbar_wait(tmem_full, 0);
+            tc_fence_after();
+        }
+#pragma unroll 1
+        for (int cb = 0; cb < BN / 32; ++cb) {
+            uint32_t r[32];
+            if (niter > 0) {
+                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r[j] = 0u;
+            }
+            if (S == 1) {
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int m = n0 + cb * 32 + j;
+                        if (m < M) O[(int64_t)m * plane + obase] = __uint_as_float(r[j]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) P[(cb * 32 + j) * kTcBM + row] = __uint_as_float(r[j]);
+            }
+        }
+        tc_fence_before();
+    }
+
+    __syncthreads();
+    if (S > 1) {
+        // ---------------------------------------------- split-K reduce via DSMEM
+        cluster_sync_all();
+        const int rows = BN / S;                         // filters owned by this rank
+        const int nlo = split * rows;
+        const uint32_t Pbase = smem_u32(smem);
+        const int64_t plane = (int64_t)Ho * Wo;
+        for (int idx = threadIdx.x; idx < rows * kTcBM; idx += kTcThreads) {
+            const int nl = nlo + idx / kTcBM, row = idx % kTcBM;
+            const int pe = p0 + row;
+            const int y = pe / Wx, x = pe - y * Wx;
+            const uint32_t off = (uint32_t)((nl * kTcBM + row) * 4);
+            float v = 0.f;
+            for (int t = 0; t < S; ++t) v += ld_dsmem_f32(mapa_shared(Pbase + off, (uint32_t)t));
+            const int m = n0 + nl;
+            if (m < M && pe < Ho * Wx && x < Wo) O[(int64_t)m * plane + (int64_t)y * Wo + x] = v;
+        }
+        cluster_sync_all();
+    }
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<BN>(tmem);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+int tc_bn(int M) {
+    if (M <= 32) return 32;
+    if (M <= 64) return 64;
+    return 128;
+}
+}  // namespace
+
+int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p) {
+    const int Ho = Wy - K + 1;
+    const int elem = bf16 ? 2 : 4;
+    const int BK = 128 / elem;
+    const int64_t Ktot = (int64_t)C * K * K;
+    const int nkb = (int)((Ktot + BK - 1) / BK);
+    const int BN = tc_bn(M);
+    const int npt = (Ho * Wx + kTcBM - 1) / kTcBM;
+    const int nft = (M + BN - 1) / BN;
+    const int tiles = npt * nft;
+    int S = 1;
+    while (S < kTcMaxSplit && tiles * S * 2 <= 2 * kNumSMs && 2 * S <= nkb && tiles * S < kNumSMs) S *= 2;
+    p->kernel = 2;
+    p->grid_x = S;
+    p->grid_y = npt;
+    p->grid_z = nft;
+    p->block_x = kTcThreads;
+    p->cluster_x = S;
+    p->tile_m = BN;
+    p->tile_n = kTcBM;
+    p->smem_bytes = tc_smem_bytes(BN);
+    const bool aligned = ((Ktot * elem) % 16 == 0) &&
+                         (F == nullptr || (reinterpret_cast<uintptr_t>(F) % 16) == 0);
+    p->tma_f = aligned ? 1 : 0;
+    return 0;
+}
+
+template <bool kTF32, int BN, bool kTmaB>
+static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tm, const void *I, int C, int Wx,
+                             int Wy, const void *F, int K, int M, float *O, cudaStream_t s) {
+    auto kern = kmtc_kernel<kTF32, BN, kTmaB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    const int BK = kTF32 ? 32 : 64;
+    const int nkb = (int)(((int64_t)C * K * K + BK - 1) / BK);
+    const int kb_per_split = (nkb + p.cluster_x - 1) / p.cluster_x;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
+    cfg.blockDim = dim3(p.block_x);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.cluster_x;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tm, I, F, C, Wx, Wy, K, M, O, kb_per_split);
+}
+
+template <bool kTF32, int BN>
+static cudaError_t launch_tc_bn(const conv_plan &p, const void *I, int C, int Wx, int Wy,
+                                const void *F, int K, int M, float *O, cudaStream_t s) {
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    if (p.tma_f) {
+        auto encode = get_encode();
+        if (!encode) return cudaErrorNotSupported;
+        const int elem = kTF32 ? 4 : 2;
+        const cuuint64_t Ktot = (cuuint64_t)C * K * K;
+        cuuint64_t dims[2] = {Ktot, (cuuint64_t)M};
+        cuuint64_t strides[1] = {Ktot * elem};
+        cuuint32_t box[2] = {(cuuint32_t)(128 / elem), (cuuint32_t)BN};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode(&tm, kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                            2, const_cast<void *>(F), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        return launch_tc<kTF32, BN, true>(p, tm, I, C, Wx, Wy, F, K, M, O, s);
+    }
+    return launch_tc<kTF32, BN, false>(p, tm, I, C, Wx, Wy, F, K, M, O, s);
+}
+
+template <bool kTF32>
+static cudaError_t launch_tc_prec(const conv_plan &p, const void *I, int C, int Wx, int Wy,
+                                  const void *F, int K, int M, float *O, cudaStream_t s) {
+    switch (p.tile_m) {
+        case 32: return launch_tc_bn<kTF32, 32>(p, I, C, Wx, Wy, F, K, M, O, s);
+        case 64: return launch_tc_bn<kTF32, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
+        default: return launch_tc_bn<kTF32, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
+    }
+}
+
+cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
+                            float *O, bool bf16, cudaStream_t s) {
+    conv_plan p;
+    plan_multi_tc(C, Wx, Wy, K, M, bf16, F, &p);
+    return bf16 ? launch_tc_prec<false>(p, I, C, Wx, Wy, F, K, M, O, s)
+                : launch_tc_prec<true>(p, I, C, Wx, Wy, F, K, M, O, s);
+}
+
+}  // namespace b200

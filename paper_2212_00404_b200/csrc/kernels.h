@@ -1,0 +1,26 @@
+// kernels.h — internal launch interface between the C ABI (abi.cu) and the
+// three kernels (KS, KM-SIMT, KM-TC).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include "../../include/b200conv.h"
+
+namespace b200 {
+
+constexpr int kNumSMs = 148;  // B200; planners size grids against it
+
+// KS: single-channel FP32 (conv_single.cu)
+int plan_single(int Wx, int Wy, int K, int M, conv_plan *p);
+cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                          cudaStream_t s);
+
+// KM-SIMT: multi-channel strict FP32 (conv_multi_simt.cu)
+int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p);
+cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
+                              float *O, cudaStream_t s);
+
+// KM-TC: multi-channel tcgen05 implicit GEMM, TF32 or BF16 (conv_multi_tc.cu)
+int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p);
+cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
+                            float *O, bool bf16, cudaStream_t s);
+
+}  // namespace b200

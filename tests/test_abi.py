@@ -1,0 +1,104 @@
+"""C-ABI library checks that need no GPU: the library builds/loads, exports every
+symbol include/b200conv.h declares, validates arguments before touching the
+device, and plans one launch per call.  (`-m "not gpu"`.)"""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from paper_2212_00404_b200 import conv
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "b200conv.h")
+
+
+def header_symbols():
+    src = open(HEADER).read()
+    return re.findall(r"B200CONV_API\s+[\w\s\*]*?\b(conv_\w+)\s*\(", src)
+
+
+def test_library_exports_every_header_symbol():
+    lib = conv.load()
+    syms = header_symbols()
+    assert len(syms) == 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(conv.EXPORTS)
+    assert conv.version() == (1 << 16)
+
+
+def test_status_strings():
+    lib = conv.load()
+    for st in range(7):
+        assert lib.conv_status_string(st)
+    assert b"unknown" in lib.conv_status_string(99)
+
+
+BAD_SHAPES = [  # (C, Wx, Wy, K, M)
+    (0, 8, 8, 3, 4), (1, 0, 8, 3, 4), (1, 8, 0, 3, 4), (1, 8, 8, 0, 4), (1, 8, 8, 3, 0),
+    (1, 8, 8, 9, 4), (1, 2, 8, 3, 4), (1, 8, 2, 3, 4), (-1, 8, 8, 3, 4),
+    (70000, 200, 200, 3, 4),      # C*Wx*Wy overflows int32
+]
+
+
+@pytest.mark.parametrize("C,Wx,Wy,K,M", BAD_SHAPES)
+def test_shape_errors_before_any_device_access(C, Wx, Wy, K, M):
+    lib = conv.load()
+    fake = 0x1000  # never dereferenced: validation rejects first
+    assert lib.conv_multi_ex(fake, C, Wx, Wy, fake, K, M, fake, 0, None) == 1
+    assert lib.conv_multi(fake, C, Wx, Wy, fake, K, M, fake) == 1
+    if C == 1:
+        assert lib.conv_single_ex(fake, Wx, Wy, fake, K, M, fake, None) == 1
+    p = conv.ConvPlan()
+    assert lib.conv_plan_multi(C, Wx, Wy, K, M, 1, ctypes.byref(p)) == 1
+
+
+def test_null_align_precision_errors():
+    lib = conv.load()
+    f = 0x1000
+    assert lib.conv_single_ex(None, 8, 8, f, 3, 4, f, None) == 2
+    assert lib.conv_multi_ex(f, 2, 8, 8, None, 3, 4, f, 1, None) == 2
+    assert lib.conv_multi_ex(f, 2, 8, 8, f, 3, 4, None, 1, None) == 2
+    assert lib.conv_single_ex(f + 2, 8, 8, f, 3, 4, f, None) == 3          # f32 needs 4-B alignment
+    assert lib.conv_multi_ex(f, 2, 8, 8, f + 2, 3, 4, f, 2, None) != 3     # bf16: 2-B is enough
+    assert lib.conv_multi_ex(f, 2, 8, 8, f + 1, 3, 4, f, 2, None) == 3
+    assert lib.conv_multi_ex(f, 2, 8, 8, f, 3, 4, f, 7, None) == 4
+    assert lib.conv_multi_ex(f, 2, 8, 8, f, 3, 4, f, -1, None) == 4
+    p = conv.ConvPlan()
+    assert lib.conv_plan_multi(2, 8, 8, 3, 4, 9, ctypes.byref(p)) == 4
+    assert lib.conv_plan_multi(2, 8, 8, 3, 4, 1, None) == 2
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_no_device_is_reported_not_faked():
+    lib = conv.load()
+    f = 0x1000
+    assert lib.conv_single_ex(f, 8, 8, f, 3, 4, f, None) == 5
+    assert lib.conv_multi_ex(f, 2, 8, 8, f, 3, 4, f, 1, None) == 5
+    with pytest.raises(conv.ConvError):
+        conv.conv_single(f, 8, 8, f, 3, 4, f)
+
+
+def test_plans_cover_every_config_with_one_launch():
+    import synth
+    for cfg in synth.SINGLE_SWEEP + [synth.PR1]:
+        p = conv.plan_single(cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"])
+        assert p["kernel"] == 0 and p["grid_x"] * p["grid_y"] * p["grid_z"] >= 1
+        Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
+        assert p["grid_x"] * p["block_x"] >= Wo
+        assert p["grid_z"] * p["tile_m"] >= cfg["M"]
+        assert p["smem_bytes"] <= 227 * 1024
+    for cfg in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
+        for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
+            p = conv.plan_multi(cfg["C"], cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"], prec)
+            assert p["kernel"] == kern
+            assert p["cluster_x"] in (1, 2, 4, 8) and p["grid_x"] == p["cluster_x"]
+            assert p["smem_bytes"] <= 227 * 1024
+            Ho = cfg["Wy"] - cfg["K"] + 1
+            assert p["grid_y"] * p["tile_n"] >= Ho * cfg["Wx"]      # wide pixels covered
+            assert p["grid_z"] * p["tile_m"] >= cfg["M"]
+            if prec != "fp32":
+                aligned = (cfg["C"] * cfg["K"] ** 2 * (2 if prec == "bf16" else 4)) % 16 == 0
+                assert p["tma_f"] == int(aligned)

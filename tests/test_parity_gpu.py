@@ -1,0 +1,237 @@
+"""Parity of the CUDA path (through the C ABI) with the fp64 CPU oracle, element
+by element, on identical seeded inputs (synth.py).  `-m gpu`.
+
+Acceptance per output (north_star):
+    |O_gpu - O_oracle| <= tau * A,   A = sum |I*F| (oracle, on the fp32 inputs)
+    tau = 1e-5 (FP32: KS, KM-SIMT), 2e-3 (TF32, KM-TC), 1e-2 (BF16, KM-TC)
+and O_gpu == 0 wherever A == 0.  On small-integer inputs every path is
+bit-exact (pin P10).  Full BASELINE sizes run in the same launch configuration
+bench.py times (same entry points, same plans)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TAU = {"fp32": 1e-5, "tf32": 2e-3, "bf16": 1e-2}
+
+
+@pytest.fixture(scope="module")
+def conv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_00404_b200 import conv as c
+    c.load()
+    return c
+
+
+def run_single(conv, I, F):
+    Id = torch.from_numpy(I).cuda()
+    Fd = torch.from_numpy(F).cuda()
+    O = conv.single(Id, Fd)
+    torch.cuda.synchronize()
+    return O.cpu().numpy().astype(np.float64)
+
+
+def run_multi(conv, I, F, prec):
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    Id = torch.from_numpy(I).cuda().to(dt)
+    Fd = torch.from_numpy(F).cuda().to(dt)
+    O = conv.multi(Id, Fd, prec)
+    torch.cuda.synchronize()
+    return O.cpu().numpy().astype(np.float64)
+
+
+def assert_parity(Og, Oo, A, tau, what=""):
+    assert Og.shape == Oo.shape, (what, Og.shape, Oo.shape)
+    err = np.abs(Og - Oo)
+    bad = err > tau * A
+    if bad.any():
+        i = np.argwhere(bad)[0]
+        raise AssertionError(f"{what}: {bad.sum()} / {bad.size} outputs out of tolerance; first at "
+                             f"{tuple(i)}: gpu={Og[tuple(i)]!r} oracle={Oo[tuple(i)]!r} "
+                             f"A={A[tuple(i)]!r} max err/A={float((err / np.maximum(A, 1e-300)).max()):.3g}")
+    zero = A == 0
+    assert np.all(Og[zero] == 0), what
+    return float((err / np.where(A > 0, A, 1)).max())
+
+
+# ------------------------------------------------------------------ single-channel (KS)
+def test_pr1_single(conv):
+    c = synth.PR1
+    I, F = synth.layer_inputs(1, c["Wx"], c["Wy"], c["K"], c["M"])
+    Oo, A = oracle.conv_single(I[0], F[:, 0])
+    Og = run_single(conv, I[0], F[:, 0])
+    assert_parity(Og, Oo, A, TAU["fp32"], "PR1")
+
+
+def test_golden_through_gpu(conv):
+    from conftest import load_golden
+    for name in ("p1_single_handworked.txt", "p2_orientation_delta.txt"):
+        g = load_golden(name)
+        Og = run_single(conv, g["I"][0].astype(np.float32), g["F"][:, 0].astype(np.float32))
+        assert np.array_equal(Og, g["O"]), name
+    g = load_golden("p3_multi_handworked.txt")
+    for prec in ("fp32", "tf32", "bf16"):
+        Og = run_multi(conv, g["I"].astype(np.float32), g["F"].astype(np.float32), prec)
+        assert np.array_equal(Og, g["O"]), prec
+
+
+@pytest.mark.parametrize("idx", range(len(synth.SINGLE_SWEEP)))
+def test_single_sweep_full_size(conv, idx):
+    c = synth.SINGLE_SWEEP[idx]
+    I, F = synth.layer_inputs(1, c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=idx)
+    Oo, A = oracle.conv_single(I[0], F[:, 0])
+    Og = run_single(conv, I[0], F[:, 0])
+    assert_parity(Og, Oo, A, TAU["fp32"], c["name"])
+
+
+SINGLE_EDGE = [  # (Wx, Wy, K, M): ragged, degenerate, generic-K, large maps
+    (5, 5, 5, 3), (1, 1, 1, 1), (9, 4, 4, 7), (300, 17, 3, 5), (33, 65, 2, 9), (20, 20, 11, 6),
+    (13, 13, 13, 2), (1000, 3, 3, 3), (64, 64, 6, 33), (257, 9, 1, 17),
+]
+
+
+@pytest.mark.parametrize("Wx,Wy,K,M", SINGLE_EDGE)
+def test_single_edge_cases(conv, Wx, Wy, K, M):
+    I = synth.uniform01(21, (Wy, Wx))
+    F = synth.uniform_pm1(22, (M, K, K))
+    Oo, A = oracle.conv_single(I, F)
+    assert_parity(run_single(conv, I, F), Oo, A, TAU["fp32"], f"single {Wx}x{Wy} K{K} M{M}")
+
+
+def test_single_positive_stress_and_ints(conv):
+    I, F = synth.layer_inputs(1, 56, 56, 7, 32, kind="positive")
+    Oo, A = oracle.conv_single(I[0], F[:, 0])
+    assert_parity(run_single(conv, I[0], F[:, 0]), Oo, A, TAU["fp32"], "positive")
+    I, F = synth.layer_inputs(1, 56, 56, 5, 32, kind="ints")
+    Oo, _ = oracle.conv_single(I[0], F[:, 0])
+    assert np.array_equal(run_single(conv, I[0], F[:, 0]), Oo)
+
+
+# ------------------------------------------------------------------ multi-channel
+MULTI = synth.MULTI_LAYERS
+
+
+@pytest.fixture(scope="module")
+def multi_oracle():
+    cache = {}
+
+    def get(i, kind="default"):
+        key = (i, kind)
+        if key not in cache:
+            c = MULTI[i]
+            I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=100 + i,
+                                      kind=kind)
+            Oo, A = oracle.conv_multi(I, F)
+            cache[key] = (I, F, Oo, A)
+        return cache[key]
+    return get
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("i", range(len(MULTI)))
+def test_multi_layers_full_size(conv, multi_oracle, i, prec):
+    I, F, Oo, A = multi_oracle(i)
+    Og = run_multi(conv, I, F, prec)
+    assert_parity(Og, Oo, A, TAU[prec], f"{MULTI[i]['name']} {prec}")
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+def test_multi_integer_inputs_bit_exact(conv, prec):
+    for (C, W, K, M) in [(64, 14, 3, 96), (3, 40, 3, 64), (96, 27, 5, 40), (512, 7, 3, 64)]:
+        I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
+        Oo, _ = oracle.conv_multi(I, F)
+        Og = run_multi(conv, I, F, prec)
+        assert np.array_equal(Og, Oo), (C, W, K, M, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+def test_multi_positive_stress(conv, prec):
+    I, F = synth.layer_inputs(256, 14, 14, 3, 64, kind="positive")
+    Oo, A = oracle.conv_multi(I, F)
+    assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"positive {prec}")
+
+
+MULTI_EDGE = [  # (C, Wx, Wy, K, M): ragged tiles, odd K*K*C, tiny/degenerate, generic K
+    (1, 9, 9, 3, 5), (2, 5, 7, 5, 3), (5, 17, 11, 3, 37), (3, 30, 30, 1, 130), (7, 6, 6, 6, 9),
+    (16, 33, 19, 2, 200), (9, 12, 12, 4, 70), (130, 9, 9, 3, 33), (4, 20, 20, 9, 16),
+    (1, 1, 1, 1, 1), (33, 3, 3, 3, 257),
+]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("C,Wx,Wy,K,M", MULTI_EDGE)
+def test_multi_edge_cases(conv, prec, C, Wx, Wy, K, M):
+    I = synth.uniform01(31, (C, Wy, Wx))
+    F = synth.uniform_pm1(32, (M, C, K, K))
+    Oo, A = oracle.conv_multi(I, F)
+    assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"edge {C},{Wx},{Wy},{K},{M} {prec}")
+
+
+def test_shard_sweep_sampled_full_size(conv):
+    """BASELINE configs[4] (14x14 C=512 M=4096 K=3) at full size, sampled outputs."""
+    c = synth.SHARD_SWEEP
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=200)
+    rng = np.random.default_rng(0)
+    Ho = c["Wy"] - c["K"] + 1
+    n = c["M"] * Ho * (c["Wx"] - c["K"] + 1)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 4000), np.arange(200), np.arange(n - 200, n)]))
+    Oo, A = oracle.conv_multi_sampled(I, F, idx)
+    for prec in ("fp32", "tf32", "bf16"):
+        Og = run_multi(conv, I, F, prec).ravel()[idx]
+        assert_parity(Og, Oo, A, TAU[prec], f"shard sweep {prec}")
+
+
+def test_multi_c1_equals_single_and_determinism(conv):
+    I = synth.uniform01(41, (1, 28, 28))
+    F = synth.uniform_pm1(42, (16, 1, 3, 3))
+    a = run_multi(conv, I, F, "fp32")
+    b = run_multi(conv, I, F, "fp32")
+    assert np.array_equal(a, b)
+    s = run_single(conv, I[0], F[:, 0])
+    Oo, A = oracle.conv_single(I[0], F[:, 0])
+    assert_parity(a, Oo, A, TAU["fp32"])
+    assert_parity(s, Oo, A, TAU["fp32"])
+    for prec in ("tf32", "bf16"):
+        c = synth.MULTI_LAYERS[6]
+        I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=7)
+        assert np.array_equal(run_multi(conv, I, F, prec), run_multi(conv, I, F, prec))
+
+
+def test_filter_shards_concatenate(conv):
+    """Filter-index sharding: F/O slices are contiguous sub-ranges."""
+    c = synth.MULTI_LAYERS[1]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=3)
+    Oo, A = oracle.conv_multi(I, F)
+    for prec in ("fp32", "tf32", "bf16"):
+        parts = [run_multi(conv, I, np.ascontiguousarray(F[a:a + 64]), prec) for a in range(0, c["M"], 64)]
+        assert_parity(np.concatenate(parts), Oo, A, TAU[prec], f"shards {prec}")
+
+
+def test_host_entry_points(conv):
+    c = synth.MULTI_LAYERS[0]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=5)
+    Oo, A = oracle.conv_multi(I, F)
+    for prec in ("fp32", "tf32"):
+        Og = conv.multi_host(torch.from_numpy(I), torch.from_numpy(F), prec).numpy().astype(np.float64)
+        assert_parity(Og, Oo, A, TAU[prec], f"host {prec}")
+    Og = conv.multi_host(torch.from_numpy(I).bfloat16(), torch.from_numpy(F).bfloat16(), "bf16")
+    assert_parity(Og.numpy().astype(np.float64), Oo, A, TAU["bf16"], "host bf16")
+    I1, F1 = synth.layer_inputs(1, 56, 56, 3, 64)
+    Oo, A = oracle.conv_single(I1[0], F1[:, 0])
+    Og = conv.single_host(torch.from_numpy(I1[0]), torch.from_numpy(F1[:, 0])).numpy().astype(np.float64)
+    assert_parity(Og, Oo, A, TAU["fp32"], "host single")
+
+
+def test_output_untouched_on_argument_error(conv):
+    O = torch.full((4, 6, 6), 7.0, device="cuda")
+    I = torch.rand(8, 8, device="cuda")
+    F = torch.rand(4, 9, 9, device="cuda")     # K=9 > 8
+    with pytest.raises(conv.ConvError):
+        conv.conv_single_ex(I, 8, 8, F, 9, 4, O)
+    torch.cuda.synchronize()
+    assert torch.all(O == 7.0)
