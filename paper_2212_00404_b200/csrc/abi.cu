@@ -3,11 +3,17 @@
 // points.  Every compute step of the hot path runs in the kernels; this file
 // only checks and launches.
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "kernels.h"
 
 using namespace b200;
+
+int b200::pdl_enabled() {
+    const char *e = getenv("B200CONV_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+}
 
 namespace {
 

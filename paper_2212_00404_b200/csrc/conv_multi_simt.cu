@@ -53,6 +53,8 @@ kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
            int M, float *__restrict__ O) {
     const int Ho = Wy - K + 1, Wo = Wx - K + 1;
     const int64_t n = (int64_t)M * Ho * Wo;
+    pdl_wait();
+    pdl_trigger();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n;
          o += (int64_t)gridDim.x * blockDim.x) {
         const int m = (int)(o / ((int64_t)Ho * Wo));
@@ -121,6 +123,8 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
+    pdl_wait();
+    pdl_trigger();
     if (nchunks > 0) load_chunk(0, 0);
     cp_async_commit();
     for (int chunk = 0; chunk < nchunks; ++chunk) {
@@ -247,13 +251,15 @@ static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx,
     cfg.blockDim = dim3(p.block_x);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = p.cluster_x;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, ch_per_split, NP);
 }
 

@@ -111,6 +111,8 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();                     // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (B = F)
@@ -358,13 +360,15 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tm, const vo
     cfg.blockDim = dim3(p.block_x);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = p.cluster_x;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, tm, I, F, C, Wx, Wy, K, M, O, kb_per_split);
 }
 

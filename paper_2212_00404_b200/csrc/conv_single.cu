@@ -4,93 +4,169 @@
 //
 //   O[m][y][x] = sum_{r,c} I[y+r][x+c] * F[m][r][c]
 //
-// B200 design (not the paper's P/Q planner):
-//  * One CTA = one output tile of TY rows x BX columns x R filters.  The
-//    paper's "both feature maps and filters are divided" option
-//    becomes the (x, y, m) grid; grids hold many waves of 148 SMs.
-//  * The halo band I[y0 .. y0+TY+K-1)[x0 .. x0+BX+K-1) is staged once in
-//    shared memory with coalesced loads (I is L2-resident: <= 200 KB).
-//  * The R*K*K filter taps live in registers ("filters fully to registers",
-//    P:665-667); every thread computes a TY x R register tile of one output
-//    column, so each staged input value feeds up to K*R FMAs.
-//  * Stores are the HBM-binding stream for K <= 3 (O is >= 94 % of all bytes
-//    for Wx >= 56): each warp store writes 32 consecutive x of one (m, y) row
-//    (128 B, fully coalesced), with the streaming .cs hint.
+// For K <= 3 the output stream (O is >= 94 % of all bytes for Wx >= 56) binds
+// to HBM; for K >= 5 the FP32 FMA pipe binds.  Design:
+//  * One CTA owns a band of TY full output rows and a chunk of filters.  Because
+//    the band spans whole rows, O[m][y0 : y0+TY][:] is ONE contiguous range of
+//    TY*Wo floats per filter.  The paper's "only the feature maps are divided
+//    ... processed by all filters" option at CTA level: the halo
+//    band I[y0 .. y0+TY+K-1) is staged once in shared memory and reused for
+//    every filter of the chunk ("FMA operations per loaded data").
+//  * Filters are processed in groups of R; their taps sit in registers
+//    ("filters fully to registers").  Each thread computes R filters
+//    x 4 consecutive pixels (16-B shared loads of the input window, sliding
+//    window reuse across the K taps of a row).
+//  * Results go to a double-buffered shared-memory image of the contiguous
+//    output range (laid out so that smem and global addresses agree mod 16 B)
+//    and leave through ONE bulk TMA store per filter (cp.async.bulk
+//    shared->global): the write stream costs no per-element instructions.
+//    The <= 3 unaligned head/tail elements of a range are stored by threads.
 #include <cstdint>
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace b200 {
 
-template <int K, int R, int TY>
-__global__ void __launch_bounds__(256)
-ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__ F, int M,
-          float *__restrict__ O) {
-    extern __shared__ float s_in[];                  // (TY+K-1) x SW
-    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
-    const int BX = blockDim.x;
-    const int SW = BX + K - 1;
-    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * TY, m0 = blockIdx.z * R;
-    const int tx = threadIdx.x;
+constexpr int kKsThreads = 256;
+constexpr int kKsWarps = kKsThreads / 32;
 
-    // stage the halo band (zero outside the map; those lanes produce no output)
-    const int n_in = (TY + K - 1) * SW;
-    for (int idx = tx; idx < n_in; idx += BX) {
-        const int rr = idx / SW, cc = idx - rr * SW;
-        const int gy = y0 + rr, gx = x0 + cc;
-        s_in[idx] = (gy < Wy && gx < Wx) ? __ldg(I + (int64_t)gy * Wx + gx) : 0.f;
+// One work item = (row-iteration, filter group): a warp computes RW output rows
+// (RW = 1 unless a row is shorter than 16 px) x R filters, lane l owning TX
+// consecutive pixels.  Warps run independently (no CTA barrier after staging):
+// each writes its tile to a warp-private double-buffered smem image of the
+// contiguous global range and lane 0 streams it out with one bulk store per
+// filter.
+template <int K, int R, int TX>
+__global__ void __launch_bounds__(kKsThreads)
+ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__ F, int M,
+          float *__restrict__ O, int m_per_cta, int TY) {
+    constexpr int KK = K * K;
+    constexpr int GS = (R * KK + 3) & ~3;            // floats per filter group (16-B rows)
+    constexpr int WN = TX + K - 1;                   // input window per lane
+    extern __shared__ __align__(16) float smem[];
+    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
+    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;      // rows per warp iteration
+    const int SW = ((TX == 1 && RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
+    const int y0 = blockIdx.y * TY;
+    const int rows = min(TY, Ho - y0);
+    const int n_ri = (rows + RW - 1) / RW;
+    const int CHW = ((RW * Wo + 3) & ~3) + 4;        // smem floats per (filter) output image
+    const int mc0 = blockIdx.x * m_per_cta;
+    const int mc1 = min(M, mc0 + m_per_cta);
+    const int ngroups = (mc1 - mc0 + R - 1) / R;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t plane = (int64_t)Ho * Wo;
+
+    float *s_w = smem;                                           // [groups][GS]
+    float *s_in = s_w + ((m_per_cta + R - 1) / R) * GS;          // (TY+K-1) x SW
+    float *s_out = s_in + (TY + K - 1) * SW + warp * 2 * R * CHW; // this warp: [2][R][CHW]
+
+    pdl_wait();
+    for (int idx = tid; idx < ngroups * GS; idx += kKsThreads) {
+        const int g = idx / GS, e = idx - g * GS;
+        const int f = e / KK, t = e - f * KK;
+        const int m = mc0 + g * R + f;
+        s_w[idx] = (f < R && m < mc1) ? __ldg(F + (int64_t)m * KK + t) : 0.f;
     }
-    // filter taps -> registers (warp-uniform addresses: broadcast loads)
-    float w[R][K * K];
-#pragma unroll
-    for (int f = 0; f < R; ++f) {
-        const bool ok = (m0 + f) < M;
-        const float *Ff = F + (int64_t)(m0 + f) * K * K;
-#pragma unroll
-        for (int t = 0; t < K * K; ++t) w[f][t] = ok ? __ldg(Ff + t) : 0.f;
+    const int hr = rows + K - 1;
+    for (int rr = warp; rr < TY + K - 1; rr += kKsWarps) {
+        const float *src = I + (int64_t)(y0 + rr) * Wx;
+        for (int cc = lane; cc < SW; cc += 32)
+            s_in[rr * SW + cc] = (rr < hr && cc < Wx) ? __ldg(src + cc) : 0.f;
     }
+    pdl_trigger();
     __syncthreads();
 
-    float acc[TY][R];
-#pragma unroll
-    for (int ty = 0; ty < TY; ++ty)
-#pragma unroll
-        for (int f = 0; f < R; ++f) acc[ty][f] = 0.f;
+    // lane -> (row within the iteration, first pixel)
+    int lrow, lx;
+    if (RW > 1) { lrow = lane / Wo; lx = lane - lrow * Wo; }
+    else        { lrow = 0;         lx = lane * TX; }
+    const bool lane_ok = (RW > 1) ? (lrow < RW) : (lx < Wo);
 
-    // input row iy feeds output row ty with filter row r = iy - ty
+    const int n_items = n_ri * ngroups;
+    int local = 0;
+    for (int it = warp; it < n_items; it += kKsWarps, ++local) {
+        const int ri = it % n_ri, g = it / n_ri;
+        float *ob = s_out + (local & 1) * R * CHW;
+        if (local >= 2) {
+            if (lane == 0) bulk_wait_read<1>();       // stores issued 2 items ago have read ob
+            __syncwarp();
+        }
+        float w[GS];
 #pragma unroll
-    for (int iy = 0; iy < TY + K - 1; ++iy) {
-        float v[K];
+        for (int q = 0; q < GS / 4; ++q) {
+            const float4 v = *reinterpret_cast<const float4 *>(s_w + g * GS + 4 * q);
+            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+        }
+        const int yb = ri * RW;                       // first band row of this iteration
+        const int nrows = min(RW, rows - yb);         // rows in this iteration
+        const int len = nrows * Wo;                   // contiguous floats per filter
+        const int m0 = mc0 + g * R;
+        const int64_t g00 = ((int64_t)m0 * Ho + y0 + yb) * Wo;   // range start of filter m0
+        const int yl = yb + lrow;
+        if (lane_ok && lrow < nrows) {
+            float acc[R][TX];
 #pragma unroll
-        for (int c = 0; c < K; ++c) v[c] = s_in[iy * SW + tx + c];
+            for (int f = 0; f < R; ++f)
 #pragma unroll
-        for (int ty = 0; ty < TY; ++ty) {
-            const int r = iy - ty;
-            if (r >= 0 && r < K) {
+                for (int j = 0; j < TX; ++j) acc[f][j] = 0.f;
 #pragma unroll
-                for (int f = 0; f < R; ++f)
+            for (int r = 0; r < K; ++r) {
+                const float *row = s_in + (yl + r) * SW + lx;
+                float win[WN];
 #pragma unroll
-                    for (int c = 0; c < K; ++c) acc[ty][f] = fmaf(v[c], w[f][r * K + c], acc[ty][f]);
+                for (int u = 0; u < WN; ++u) win[u] = row[u];
+#pragma unroll
+                for (int c = 0; c < K; ++c)
+#pragma unroll
+                    for (int f = 0; f < R; ++f)
+#pragma unroll
+                        for (int j = 0; j < TX; ++j)
+                            acc[f][j] = fmaf(win[j + c], w[f * KK + r * K + c], acc[f][j]);
+            }
+            const int e = lrow * Wo + lx;
+#pragma unroll
+            for (int f = 0; f < R; ++f) {
+                const int sh = (int)((g00 + (int64_t)f * plane) & 3);
+                float *d = ob + f * CHW + sh + e;
+#pragma unroll
+                for (int j = 0; j < TX; ++j)
+                    if (lx + j < Wo) d[j] = acc[f][j];
             }
         }
-    }
-
-    const int x = x0 + tx;
-    if (x < Wo) {
-#pragma unroll
-        for (int f = 0; f < R; ++f) {
-            if (m0 + f >= M) break;
-            float *Of = O + (int64_t)(m0 + f) * Ho * Wo + x;
-#pragma unroll
-            for (int ty = 0; ty < TY; ++ty) {
-                const int y = y0 + ty;
-                if (y < Ho) st_cs(Of + (int64_t)y * Wo, acc[ty][f]);
+        fence_proxy_async_smem();                     // smem image -> visible to the bulk copy
+        __syncwarp();
+        if (lane == 0) {
+            for (int f = 0; f < R && m0 + f < mc1; ++f) {
+                const int64_t g0 = g00 + (int64_t)f * plane;
+                const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = (g0 + len) & ~(int64_t)3;
+                if (a1 > a0)
+                    bulk_store(O + a0, ob + f * CHW + (int)(g0 & 3) + (int)(a0 - g0),
+                               (uint32_t)((a1 - a0) * 4));
             }
+            bulk_commit();
+        }
+        // <= 3 head and <= 3 tail elements per filter (or a whole range < 8 floats)
+        for (int t = lane; t < 8 * R; t += 32) {
+            const int f = t >> 3, j = t & 7;
+            if (m0 + f >= mc1) continue;
+            const int64_t g0 = g00 + (int64_t)f * plane;
+            const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = (g0 + len) & ~(int64_t)3;
+            int64_t gi = -1;
+            if (a1 > a0) {
+                if (j < 4) { if (g0 + j < a0) gi = g0 + j; }
+                else if (a1 + (j - 4) < g0 + len) gi = a1 + (j - 4);
+            } else if (j < len) {
+                gi = g0 + j;
+            }
+            if (gi >= 0) O[gi] = ob[f * CHW + (int)(g0 & 3) + (int)(gi - g0)];
         }
     }
+    if (lane == 0) bulk_wait<0>();                    // keep smem alive until the copies finish
 }
 
-// Generic-K fallback (any K, e.g. K = Wx = Wy): no staging, loads through L1.
+// Generic fallback (any K, e.g. K = Wx = Wy, or rows too wide for smem): no
+// staging, loads through L1.
 template <int R, int TY>
 __global__ void __launch_bounds__(256)
 ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__ F, int K,
@@ -98,6 +174,8 @@ ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__re
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     const int x0 = blockIdx.x * blockDim.x, y0 = blockIdx.y * TY, m0 = blockIdx.z * R;
     const int x = x0 + threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
     if (x >= Wo) return;
     float acc[TY][R];
 #pragma unroll
@@ -124,73 +202,124 @@ ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__re
 }
 
 namespace {
-struct KsCfg { int R, TY; };
-// (R filters, TY rows) per thread: registers = R*K*K taps + TY*R accumulators.
-KsCfg ks_cfg(int K) {
-    switch (K) {
-        case 1: return {8, 8};
-        case 2: return {8, 4};
-        case 3: return {8, 4};
-        case 4: return {4, 8};
-        case 5: return {4, 8};
-        case 6: return {2, 8};
-        case 7: return {2, 8};
-        default: return {4, 4};
-    }
-}
-int ks_bx(int Wo) {
-    int bx = ((Wo + 31) / 32) * 32;
-    return bx > 256 ? 256 : bx;
+constexpr int kKsTargetCtas = 4 * kNumSMs;
+constexpr int kKsMaxSmem = 100 * 1024;
+
+int ks_R(int K) { return K <= 3 ? 4 : (K <= 5 ? 2 : 1); }
+int ks_TX(int Wo) { return (Wo + 31) / 32; }
+int ks_smem(int K, int R, int TX, int TY, int Wx, int Wo, int m_per) {
+    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;
+    const int SW = ((TX == 1 && RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
+    const int GS = (R * K * K + 3) & ~3;
+    const int CHW = ((RW * Wo + 3) & ~3) + 4;
+    return (((m_per + R - 1) / R) * GS + (TY + K - 1) * SW + kKsWarps * 2 * R * CHW) * 4;
 }
 }  // namespace
 
 int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
-    const KsCfg c = ks_cfg(K);
-    const int bx = ks_bx(Wo);
+    p->cluster_x = 1;
+    p->tma_f = 0;
+    const int TX = ks_TX(Wo);
+    if (K <= 7 && TX <= 8) {
+        const int R = ks_R(K);
+        int TY = Ho < 16 ? Ho : 16;
+        const int bands = (Ho + TY - 1) / TY;
+        const int max_chunks = (M + R - 1) / R;
+        int nmc = (kKsTargetCtas + bands - 1) / bands;
+        nmc = nmc < 1 ? 1 : (nmc > max_chunks ? max_chunks : nmc);
+        int m_per = (M + nmc - 1) / nmc;
+        m_per = ((m_per + R - 1) / R) * R;
+        p->kernel = 0;
+        p->block_x = kKsThreads;
+        p->grid_x = (M + m_per - 1) / m_per;
+        p->grid_y = bands;
+        p->grid_z = 1;
+        p->tile_m = m_per;                               // filters per CTA (groups of R)
+        p->tile_n = TY;                                  // output rows per CTA band (full width)
+        p->smem_bytes = ks_smem(K, R, TX, TY, Wx, Wo, m_per);
+        if (p->smem_bytes <= kKsMaxSmem) return 0;
+    }
+    // generic fallback: (x, y, m) tiles of 1 column x 4 rows x 4 filters per thread
+    const int bx = Wo >= 128 ? 128 : ((Wo + 31) / 32) * 32;
     p->kernel = 0;
     p->block_x = bx;
     p->grid_x = (Wo + bx - 1) / bx;
-    p->grid_y = (Ho + c.TY - 1) / c.TY;
-    p->grid_z = (M + c.R - 1) / c.R;
-    p->cluster_x = 1;
-    p->tile_m = c.R;
-    p->tile_n = bx * c.TY;
-    p->smem_bytes = (K <= 7) ? (c.TY + K - 1) * (bx + K - 1) * 4 : 0;
-    p->tma_f = 0;
+    p->grid_y = (Ho + 3) / 4;
+    p->grid_z = (M + 3) / 4;
+    p->tile_m = 4;
+    p->tile_n = -1;                                      // marks the generic kernel
+    p->smem_bytes = 0;
     return 0;
 }
 
-template <int K>
+static cudaLaunchAttribute pdl_attr() {
+    cudaLaunchAttribute a;
+    a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a.val.programmaticStreamSerializationAllowed = pdl_enabled();
+    return a;
+}
+
+template <int K, int TX>
 static cudaError_t launch_ks(const conv_plan &p, const float *I, int Wx, int Wy, const float *F,
                              int M, float *O, cudaStream_t s) {
-    constexpr int R = (K == 1 || K == 2 || K == 3) ? 8 : (K == 4 || K == 5) ? 4 : 2;
-    constexpr int TY = (K == 2 || K == 3) ? 4 : 8;
-    auto kern = ks_kernel<K, R, TY>;
-    if (p.smem_bytes > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
-    kern<<<dim3(p.grid_x, p.grid_y, p.grid_z), p.block_x, p.smem_bytes, s>>>(I, Wx, Wy, F, M, O);
-    return cudaGetLastError();
+    constexpr int R = K <= 3 ? 4 : (K <= 5 ? 2 : 1);
+    auto kern = ks_kernel<K, R, TX>;
+    if (p.smem_bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             p.smem_bytes);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
+    cfg.blockDim = dim3(p.block_x);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1] = {pdl_attr()};
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, I, Wx, Wy, F, M, O, p.tile_m, p.tile_n);
+}
+
+template <int K>
+static cudaError_t launch_ks_v(const conv_plan &p, const float *I, int Wx, int Wy, const float *F,
+                               int M, float *O, cudaStream_t s) {
+    switch (ks_TX(Wx - K + 1)) {
+        case 1: return launch_ks<K, 1>(p, I, Wx, Wy, F, M, O, s);
+        case 2: return launch_ks<K, 2>(p, I, Wx, Wy, F, M, O, s);
+        case 3: return launch_ks<K, 3>(p, I, Wx, Wy, F, M, O, s);
+        case 4: return launch_ks<K, 4>(p, I, Wx, Wy, F, M, O, s);
+        case 5: return launch_ks<K, 5>(p, I, Wx, Wy, F, M, O, s);
+        case 6: return launch_ks<K, 6>(p, I, Wx, Wy, F, M, O, s);
+        case 7: return launch_ks<K, 7>(p, I, Wx, Wy, F, M, O, s);
+        default: return launch_ks<K, 8>(p, I, Wx, Wy, F, M, O, s);
+    }
 }
 
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                           cudaStream_t s) {
     conv_plan p;
     plan_single(Wx, Wy, K, M, &p);
-    switch (K) {
-        case 1: return launch_ks<1>(p, I, Wx, Wy, F, M, O, s);
-        case 2: return launch_ks<2>(p, I, Wx, Wy, F, M, O, s);
-        case 3: return launch_ks<3>(p, I, Wx, Wy, F, M, O, s);
-        case 4: return launch_ks<4>(p, I, Wx, Wy, F, M, O, s);
-        case 5: return launch_ks<5>(p, I, Wx, Wy, F, M, O, s);
-        case 6: return launch_ks<6>(p, I, Wx, Wy, F, M, O, s);
-        case 7: return launch_ks<7>(p, I, Wx, Wy, F, M, O, s);
-        default: {
-            ks_kernel_generic<4, 4><<<dim3(p.grid_x, p.grid_y, p.grid_z), p.block_x, 0, s>>>(
-                I, Wx, Wy, F, K, M, O);
-            return cudaGetLastError();
+    if (p.tile_n > 0) {
+        switch (K) {
+            case 1: return launch_ks_v<1>(p, I, Wx, Wy, F, M, O, s);
+            case 2: return launch_ks_v<2>(p, I, Wx, Wy, F, M, O, s);
+            case 3: return launch_ks_v<3>(p, I, Wx, Wy, F, M, O, s);
+            case 4: return launch_ks_v<4>(p, I, Wx, Wy, F, M, O, s);
+            case 5: return launch_ks_v<5>(p, I, Wx, Wy, F, M, O, s);
+            case 6: return launch_ks_v<6>(p, I, Wx, Wy, F, M, O, s);
+            case 7: return launch_ks_v<7>(p, I, Wx, Wy, F, M, O, s);
+            default: break;
         }
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
+    cfg.blockDim = dim3(p.block_x);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1] = {pdl_attr()};
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ks_kernel_generic<4, 4>, I, Wx, Wy, F, K, M, O);
 }
 
 }  // namespace b200

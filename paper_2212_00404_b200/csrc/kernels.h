@@ -8,6 +8,9 @@ namespace b200 {
 
 constexpr int kNumSMs = 148;  // B200; planners size grids against it
 
+// Programmatic dependent launch on/off (env B200CONV_PDL=0 disables it).
+int pdl_enabled();
+
 // KS: single-channel FP32 (conv_single.cu)
 int plan_single(int Wx, int Wy, int K, int M, conv_plan *p);
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
