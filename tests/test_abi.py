@@ -87,8 +87,9 @@ def test_plans_cover_every_config_with_one_launch():
         p = conv.plan_single(cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"])
         assert p["kernel"] == 0 and p["grid_x"] * p["grid_y"] * p["grid_z"] >= 1
         Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
-        assert p["grid_x"] * p["block_x"] >= Wo
-        assert p["grid_z"] * p["tile_m"] >= cfg["M"]
+        assert p["tile_n"] > 0, "every BASELINE single-channel config uses the band kernel"
+        assert p["grid_x"] * p["tile_m"] >= cfg["M"]          # filter chunks
+        assert p["grid_y"] * p["tile_n"] >= Ho                # full-width row bands
         assert p["smem_bytes"] <= 227 * 1024
     for cfg in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
         for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
