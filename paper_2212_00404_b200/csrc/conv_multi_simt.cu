@@ -27,17 +27,6 @@
 
 namespace b200 {
 
-namespace {
-__device__ __forceinline__ void cp_async4(float *dst, const float *src, bool pred) {
-    const uint32_t d = smem_u32(dst);
-    const int sz = pred ? 4 : 0;                    // src-size 0 -> zero fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(sz)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-}  // namespace
 
 constexpr int kSimtBM = 64;
 constexpr int kSimtBN = 128;

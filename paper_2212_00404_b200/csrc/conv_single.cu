@@ -30,27 +30,30 @@ namespace b200 {
 constexpr int kKsThreads = 256;
 constexpr int kKsWarps = kKsThreads / 32;
 
-// One work item = (row-iteration, filter group): a warp computes RW output rows
-// (RW = 1 unless a row is shorter than 16 px) x R filters, lane l owning TX
-// consecutive pixels.  Warps run independently (no CTA barrier after staging):
-// each writes its tile to a warp-private double-buffered smem image of the
-// contiguous global range and lane 0 streams it out with one bulk store per
-// filter.
-template <int K, int R, int TX>
+// One work item = (row block, filter group): a warp computes RI output rows
+// x R filters.  Normal mode (rows >= 16 px): lane l owns TX consecutive pixels of
+// RR rows (vertical register blocking: an input row feeds up to min(RR, K)
+// output rows).  Small-map mode (TX == 1, Wo <= 16): the warp's lanes cover
+// RW = 32 / Wo whole rows, one pixel each.  Warps run independently after the
+// staging barrier: each writes its tile into a warp-private double-buffered
+// smem image of the contiguous global range O[m][y : y+RI][:], and lanes
+// 0..R-1 each stream one filter's range out with a bulk store.
+template <int K, int R, int TX, int RR>
 __global__ void __launch_bounds__(kKsThreads)
 ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__ F, int M,
           float *__restrict__ O, int m_per_cta, int TY) {
     constexpr int KK = K * K;
     constexpr int GS = (R * KK + 3) & ~3;            // floats per filter group (16-B rows)
-    constexpr int WN = TX + K - 1;                   // input window per lane
+    constexpr int WN = TX + K - 1;                   // input window per lane and row
     extern __shared__ __align__(16) float smem[];
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
-    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;      // rows per warp iteration
-    const int SW = ((TX == 1 && RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
+    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;      // small-map rows per warp
+    const int RI = RW > 1 ? RW : RR;                          // output rows per item
+    const int SW = ((RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
     const int y0 = blockIdx.y * TY;
     const int rows = min(TY, Ho - y0);
-    const int n_ri = (rows + RW - 1) / RW;
-    const int CHW = ((RW * Wo + 3) & ~3) + 4;        // smem floats per (filter) output image
+    const int n_ri = (rows + RI - 1) / RI;
+    const int CHW = ((RI * Wo + 3) & ~3) + 4;        // smem floats per (filter) output image
     const int mc0 = blockIdx.x * m_per_cta;
     const int mc1 = min(M, mc0 + m_per_cta);
     const int ngroups = (mc1 - mc0 + R - 1) / R;
@@ -62,26 +65,34 @@ ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__
     float *s_out = s_in + (TY + K - 1) * SW + warp * 2 * R * CHW; // this warp: [2][R][CHW]
 
     pdl_wait();
+    // stage taps and the halo band with fire-and-forget cp.async (zero-filled
+    // outside the map), one wait for all of them
     for (int idx = tid; idx < ngroups * GS; idx += kKsThreads) {
         const int g = idx / GS, e = idx - g * GS;
         const int f = e / KK, t = e - f * KK;
         const int m = mc0 + g * R + f;
-        s_w[idx] = (f < R && m < mc1) ? __ldg(F + (int64_t)m * KK + t) : 0.f;
+        const bool ok = f < R && m < mc1;
+        cp_async4(s_w + idx, ok ? F + (int64_t)m * KK + t : F, ok);
     }
     const int hr = rows + K - 1;
     for (int rr = warp; rr < TY + K - 1; rr += kKsWarps) {
         const float *src = I + (int64_t)(y0 + rr) * Wx;
-        for (int cc = lane; cc < SW; cc += 32)
-            s_in[rr * SW + cc] = (rr < hr && cc < Wx) ? __ldg(src + cc) : 0.f;
+        for (int cc = lane; cc < SW; cc += 32) {
+            const bool ok = rr < hr && cc < Wx;
+            cp_async4(s_in + rr * SW + cc, ok ? src + cc : I, ok);
+        }
     }
+    cp_async_commit();
     pdl_trigger();
+    cp_async_wait<0>();
     __syncthreads();
 
-    // lane -> (row within the iteration, first pixel)
+    // lane -> (row within the item, first pixel)
     int lrow, lx;
     if (RW > 1) { lrow = lane / Wo; lx = lane - lrow * Wo; }
     else        { lrow = 0;         lx = lane * TX; }
     const bool lane_ok = (RW > 1) ? (lrow < RW) : (lx < Wo);
+    const bool lane_full = (RW > 1) || (lx + TX <= Wo);       // no per-pixel bounds checks
 
     const int n_items = n_ri * ngroups;
     int local = 0;
@@ -89,64 +100,83 @@ ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__
         const int ri = it % n_ri, g = it / n_ri;
         float *ob = s_out + (local & 1) * R * CHW;
         if (local >= 2) {
-            if (lane == 0) bulk_wait_read<1>();       // stores issued 2 items ago have read ob
+            if (lane < R) bulk_wait_read<1>();        // this lane's store of 2 items ago read ob
             __syncwarp();
         }
-        float w[GS];
-#pragma unroll
-        for (int q = 0; q < GS / 4; ++q) {
-            const float4 v = *reinterpret_cast<const float4 *>(s_w + g * GS + 4 * q);
-            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-        }
-        const int yb = ri * RW;                       // first band row of this iteration
-        const int nrows = min(RW, rows - yb);         // rows in this iteration
+        const int yb = ri * RI;                       // first band row of this item
+        const int nrows = min(RI, rows - yb);         // rows in this item
         const int len = nrows * Wo;                   // contiguous floats per filter
         const int m0 = mc0 + g * R;
         const int64_t g00 = ((int64_t)m0 * Ho + y0 + yb) * Wo;   // range start of filter m0
-        const int yl = yb + lrow;
         if (lane_ok && lrow < nrows) {
-            float acc[R][TX];
+            float w[GS];
 #pragma unroll
-            for (int f = 0; f < R; ++f)
+            for (int q = 0; q < GS / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4 *>(s_w + g * GS + 4 * q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
+            constexpr int RL = RR;                    // rows computed per lane (1 in small mode)
+            const int nr = (RW > 1) ? 1 : nrows;      // valid rows of this lane's block
+            float acc[RL][R][TX];
 #pragma unroll
-                for (int j = 0; j < TX; ++j) acc[f][j] = 0.f;
+            for (int q = 0; q < RL; ++q)
 #pragma unroll
-            for (int r = 0; r < K; ++r) {
-                const float *row = s_in + (yl + r) * SW + lx;
+                for (int f = 0; f < R; ++f)
+#pragma unroll
+                    for (int j = 0; j < TX; ++j) acc[q][f][j] = 0.f;
+            const float *base = s_in + (yb + lrow) * SW + lx;
+#pragma unroll
+            for (int ir = 0; ir < RL + K - 1; ++ir) {
                 float win[WN];
 #pragma unroll
-                for (int u = 0; u < WN; ++u) win[u] = row[u];
+                for (int u = 0; u < WN; ++u) win[u] = base[ir * SW + u];
 #pragma unroll
-                for (int c = 0; c < K; ++c)
+                for (int q = 0; q < RL; ++q) {
+                    const int r = ir - q;             // filter row feeding output row q
+                    if (r >= 0 && r < K) {
 #pragma unroll
-                    for (int f = 0; f < R; ++f)
+                        for (int c = 0; c < K; ++c)
 #pragma unroll
-                        for (int j = 0; j < TX; ++j)
-                            acc[f][j] = fmaf(win[j + c], w[f * KK + r * K + c], acc[f][j]);
+                            for (int f = 0; f < R; ++f)
+#pragma unroll
+                                for (int j = 0; j < TX; ++j)
+                                    acc[q][f][j] = fmaf(win[j + c], w[f * KK + r * K + c], acc[q][f][j]);
+                    }
+                }
             }
             const int e = lrow * Wo + lx;
 #pragma unroll
             for (int f = 0; f < R; ++f) {
-                const int sh = (int)((g00 + (int64_t)f * plane) & 3);
-                float *d = ob + f * CHW + sh + e;
+                float *d = ob + f * CHW + (int)((g00 + (int64_t)f * plane) & 3) + e;
 #pragma unroll
-                for (int j = 0; j < TX; ++j)
-                    if (lx + j < Wo) d[j] = acc[f][j];
+                for (int q = 0; q < RL; ++q) {
+                    if (q < nr) {
+                        if (lane_full) {
+#pragma unroll
+                            for (int j = 0; j < TX; ++j) d[q * Wo + j] = acc[q][f][j];
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < TX; ++j)
+                                if (lx + j < Wo) d[q * Wo + j] = acc[q][f][j];
+                        }
+                    }
+                }
             }
         }
         fence_proxy_async_smem();                     // smem image -> visible to the bulk copy
         __syncwarp();
-        if (lane == 0) {
-            for (int f = 0; f < R && m0 + f < mc1; ++f) {
-                const int64_t g0 = g00 + (int64_t)f * plane;
+        // lane f < R: bulk store of filter f's 16-B aligned body; all lanes: the
+        // <= 3 head and <= 3 tail elements (or a whole range shorter than 8)
+        if (lane < R) {
+            if (m0 + lane < mc1) {
+                const int64_t g0 = g00 + (int64_t)lane * plane;
                 const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = (g0 + len) & ~(int64_t)3;
                 if (a1 > a0)
-                    bulk_store(O + a0, ob + f * CHW + (int)(g0 & 3) + (int)(a0 - g0),
+                    bulk_store(O + a0, ob + lane * CHW + (int)(g0 & 3) + (int)(a0 - g0),
                                (uint32_t)((a1 - a0) * 4));
             }
             bulk_commit();
         }
-        // <= 3 head and <= 3 tail elements per filter (or a whole range < 8 floats)
         for (int t = lane; t < 8 * R; t += 32) {
             const int f = t >> 3, j = t & 7;
             if (m0 + f >= mc1) continue;
@@ -162,7 +192,7 @@ ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__
             if (gi >= 0) O[gi] = ob[f * CHW + (int)(g0 & 3) + (int)(gi - g0)];
         }
     }
-    if (lane == 0) bulk_wait<0>();                    // keep smem alive until the copies finish
+    if (lane < R) bulk_wait<0>();                     // keep smem alive until the copies finish
 }
 
 // Generic fallback (any K, e.g. K = Wx = Wy, or rows too wide for smem): no
@@ -203,15 +233,19 @@ ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__re
 
 namespace {
 constexpr int kKsTargetCtas = 4 * kNumSMs;
-constexpr int kKsMaxSmem = 100 * 1024;
+constexpr int kKsMaxSmem = 110 * 1024;
 
-int ks_R(int K) { return K <= 3 ? 4 : (K <= 5 ? 2 : 1); }
+// (R filters, RR rows) per lane and item: K=1 store-bound -> more filters;
+// K>=5 FMA-bound -> more rows (an input row feeds min(RR, K) output rows)
+__host__ __device__ constexpr int ks_R(int K) { return K <= 1 ? 4 : (K <= 5 ? 2 : 1); }
+__host__ __device__ constexpr int ks_RR(int K) { return K <= 1 ? 1 : (K <= 5 ? 2 : 4); }
 int ks_TX(int Wo) { return (Wo + 31) / 32; }
 int ks_smem(int K, int R, int TX, int TY, int Wx, int Wo, int m_per) {
     const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;
-    const int SW = ((TX == 1 && RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
+    const int RI = RW > 1 ? RW : ks_RR(K);
+    const int SW = ((RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
     const int GS = (R * K * K + 3) & ~3;
-    const int CHW = ((RW * Wo + 3) & ~3) + 4;
+    const int CHW = ((RI * Wo + 3) & ~3) + 4;
     return (((m_per + R - 1) / R) * GS + (TY + K - 1) * SW + kKsWarps * 2 * R * CHW) * 4;
 }
 }  // namespace
@@ -263,8 +297,7 @@ static cudaLaunchAttribute pdl_attr() {
 template <int K, int TX>
 static cudaError_t launch_ks(const conv_plan &p, const float *I, int Wx, int Wy, const float *F,
                              int M, float *O, cudaStream_t s) {
-    constexpr int R = K <= 3 ? 4 : (K <= 5 ? 2 : 1);
-    auto kern = ks_kernel<K, R, TX>;
+    auto kern = ks_kernel<K, ks_R(K), TX, ks_RR(K)>;
     if (p.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              p.smem_bytes);
