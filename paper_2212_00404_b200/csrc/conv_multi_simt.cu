@@ -90,7 +90,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int ch_begin = split * ch_per_split;
     const int ch_end = min(C, ch_begin + ch_per_split);
     const int nchunks = ch_end > ch_begin ? (ch_end - ch_begin + CB - 1) / CB : 0;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int tn = tid % TNS, tm = tid / TNS;
     // 16-B copies of F rows when every row start of every chunk is 16-B aligned
     const bool vec_f = ((Ktot & 3) == 0) && ((CK & 3) == 0) && ((ch_per_split * KK & 3) == 0) &&

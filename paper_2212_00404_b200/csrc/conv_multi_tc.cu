@@ -11,18 +11,25 @@
 // ("along the dimension ch first"), so B is F itself: a TMA tensor
 // map loads [BN filters] x [128 B of k] boxes with the 128-B swizzle straight
 // into the canonical K-major UMMA layout (the paper's stride-fixed segment S,
-// P:603-612, becomes one 128-B TMA row).  A is gathered by four warps from the
-// L2-resident input into the same swizzled layout (one pixel row per thread,
-// 32-lane coalesced loads), fenced into the async proxy, and handed to the MMA
-// through an mbarrier ring.  Pixels go on the 128-lane M side so the epilogue
-// (tcgen05.ld -> registers -> st.global) writes 32 consecutive pixels per warp
-// instruction, coalesced.  Small layers split the k loop over a thread-block
-// cluster and reduce the partial tiles through DSMEM in fixed rank order.
+// P:603-612, becomes one 128-B TMA row).
 //
-// Warp roles (192 threads):
-//   warp 0      TMA producer of B (F tiles)            [elected lane]
-//   warp 1      TMEM allocator + MMA issuer            [elected lane]
-//   warps 2..5  im2col gather of A, then epilogue      [128 threads]
+// A is never materialised in global memory.  For every k-block the TMA
+// producer also loads the input "patch" of the channels that k-block touches:
+// with wide-pixel indexing the pixels a 128-pixel tile needs from one channel
+// form ONE contiguous range I[ch][p0 .. p0 + 128 + (K-1)*Wx + K-1), fetched by
+// 1-D TMA boxes (any alignment, zero fill past the end).  Eight gather warps
+// then expand the patch into the swizzled im2col tile with conflict-free
+// shared loads (one pixel row per thread pair), fence it into the async
+// proxy and arrive on the stage's mbarrier; one thread issues tcgen05.mma.
+// Pixels sit on the 128-lane M side, so the epilogue (tcgen05.ld -> registers
+// -> st.global) writes 32 consecutive pixels per warp instruction.  Small
+// layers split the k loop over a thread-block cluster and reduce the partial
+// tiles through DSMEM in fixed rank order (deterministic, O written once).
+//
+// Warp roles (320 threads):
+//   warp 0      TMA producer: F tile (B) + input patch      [elected lane]
+//   warp 1      TMEM allocator + MMA issuer                  [elected lane]
+//   warps 2..9  im2col build of A (2 threads per pixel row), then epilogue
 #include <cstdint>
 #include <cstring>
 #include <type_traits>
@@ -33,10 +40,10 @@
 
 namespace b200 {
 
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;
 constexpr int kTcBM = 128;            // pixels per tile (UMMA M)
-constexpr int kTcStages = 4;
 constexpr int kTcMaxSplit = 8;
+constexpr int kTcSmemMax = 225 * 1024;
 
 template <bool kTF32>
 struct TcTraits {
@@ -47,9 +54,37 @@ struct TcTraits {
     static constexpr uint32_t kFmt = kTF32 ? 2u : 1u; // instr-desc a/b format
 };
 
-__host__ __device__ constexpr int tc_stage_bytes(int BN) { return kTcBM * 128 + BN * 128; }
-__host__ __device__ constexpr int tc_smem_bytes(int BN) {
-    return 1024 /*align slack*/ + kTcStages * tc_stage_bytes(BN) + 256 /*barriers*/;
+// Per-launch geometry shared by host and device.
+struct TcGeom {
+    int np;       // patch length per channel (elements)
+    int pb;       // 1-D TMA box (elements)
+    int nbox;     // boxes per channel
+    int npp;      // patch stride per channel in smem (elements) = nbox * pb
+    int pch;      // max channels touched by one k-block
+    int patch_bytes;
+    int stages;
+    int stage_bytes;
+    int smem;
+};
+
+__host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool patch) {
+    TcGeom g;
+    const int BK = 128 / elem;
+    // a box must start 16-B aligned in global memory: the patch starts up to
+    // 16/elem - 1 elements before the channel's first pixel
+    g.np = kTcBM + (K - 1) * Wx + (K - 1) + 16 / elem - 1;
+    const int align = 128 / elem;             // TMA smem destinations: 128-B aligned
+    const int npa = (g.np + align - 1) / align * align;
+    g.pb = npa < 256 ? npa : 256;
+    g.nbox = (g.np + g.pb - 1) / g.pb;
+    g.npp = g.nbox * g.pb;
+    g.pch = (BK + K * K - 1) / (K * K) + 1;
+    g.patch_bytes = patch ? ((g.pch * g.npp * elem + 1023) & ~1023) : 0;
+    g.stage_bytes = kTcBM * 128 + BN * 128 + g.patch_bytes;
+    int st = (kTcSmemMax - 1024 - 512) / g.stage_bytes;
+    g.stages = st > 4 ? 4 : st;
+    g.smem = 1024 + g.stages * g.stage_bytes + 512;
+    return g;
 }
 
 // Byte offset of 16-B chunk j of row g in a K-major SWIZZLE_128B tile.
@@ -57,16 +92,16 @@ __device__ __forceinline__ uint32_t sw128_off(int g, int j) {
     return (uint32_t)((g >> 3) * 1024 + (g & 7) * 128 + ((j ^ (g & 7)) << 4));
 }
 
-template <bool kTF32, int BN, bool kTmaB>
+template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 __global__ void __launch_bounds__(kTcThreads, 1)
-kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ Iv,
-            const void *__restrict__ Fv, int C, int Wx, int Wy, int K, int M,
-            float *__restrict__ O, int kb_per_split) {
+kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
+            const void *__restrict__ Iv, const void *__restrict__ Fv, int C, int Wx, int Wy,
+            int K, int M, float *__restrict__ O, int kb_per_split) {
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
     constexpr int BK = Tr::kBK;
-    constexpr int STAGE = tc_stage_bytes(BN);
     constexpr int A_BYTES = kTcBM * 128;
+    constexpr int B_BYTES = BN * 128;
     constexpr uint32_t IDESC = umma_idesc(Tr::kFmt, kTcBM, BN);
 
     const T *__restrict__ I = static_cast<const T *>(Iv);
@@ -77,6 +112,9 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
     const int64_t CHW = (int64_t)C * HW;
     const int Ho = Wy - K + 1, Wo = Wx - K + 1;
     const int nkb = (Ktot + BK - 1) / BK;
+    const TcGeom geo = tc_geom(Wx, K, BN, Tr::kElem, kPatch);
+    const int NS = geo.stages;
+    const int STAGE = geo.stage_bytes;
 
     const int S = gridDim.x;
     const int split = blockIdx.x;
@@ -89,22 +127,25 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTcStages * STAGE);
-    uint64_t *empty = full + kTcStages;
-    uint64_t *tmem_full = empty + kTcStages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);   // A+B ready (MMA)
+    uint64_t *pfull = full + 4;                                          // patch landed
+    uint64_t *empty = pfull + 4;                                         // MMA done with stage
+    uint64_t *tmem_full = empty + 4;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(&full[s], kTmaB ? 5 : 4);       // 4 gather warps (+1 TMA arrive.expect_tx)
-            mbar_init(&empty[s], 1);                  // tcgen05.commit
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 8 + (kTmaB ? 1 : 0));   // 8 gather warps (+1 TMA expect_tx)
+            mbar_init(&pfull[s], 1);
+            mbar_init(&empty[s], 1);                    // tcgen05.commit
         }
         mbar_init(tmem_full, 1);
         fence_mbar_init();
         if (kTmaB) tma_prefetch_desc(&tmapF);
+        if (kPatch) tma_prefetch_desc(&tmapI);
     }
     if (warp == 1) tmem_alloc<BN>(tmem_slot);
     tc_fence_before();
@@ -115,22 +156,38 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
     pdl_trigger();
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer (B = F)
-        if (kTmaB && lane == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
             for (int i = 0; i < niter; ++i) {
-                const int s = i % kTcStages;
-                mbar_wait(&empty[s], ((i / kTcStages) & 1) ^ 1);
-                uint8_t *b_s = smem + s * STAGE + A_BYTES;
-                mbar_arrive_expect_tx(&full[s], BN * 128);
-                tma_load_2d(b_s, &tmapF, &full[s], (kb0 + i) * BK, n0);
+                const int s = i % NS;
+                mbar_wait(&empty[s], ((i / NS) & 1) ^ 1);
+                uint8_t *st = smem + s * STAGE;
+                if (kPatch) {
+                    const int k0 = (kb0 + i) * BK;
+                    const int ch_lo = k0 / KK;
+                    const int ch_hi = min(C - 1, (min(k0 + BK, Ktot) - 1) / KK);
+                    const int nch = ch_hi - ch_lo + 1;
+                    mbar_arrive_expect_tx(&pfull[s], (uint32_t)(nch * geo.npp * Tr::kElem));
+                    T *patch = reinterpret_cast<T *>(st + A_BYTES + B_BYTES);
+                    for (int j = 0; j < nch; ++j) {
+                        const int start = ((ch_lo + j) * HW + p0) & ~(16 / Tr::kElem - 1);
+                        for (int b = 0; b < geo.nbox; ++b)
+                            tma_load_1d(patch + j * geo.npp + b * geo.pb, &tmapI, &pfull[s],
+                                        start + b * geo.pb);
+                    }
+                }
+                if (kTmaB) {
+                    mbar_arrive_expect_tx(&full[s], B_BYTES);
+                    tma_load_2d(st + A_BYTES, &tmapF, &full[s], (kb0 + i) * BK, n0);
+                }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
             for (int i = 0; i < niter; ++i) {
-                const int s = i % kTcStages;
-                mbar_wait(&full[s], (i / kTcStages) & 1);
+                const int s = i % NS;
+                mbar_wait(&full[s], (i / NS) & 1);
                 tc_fence_after();
                 const uint32_t a_addr = smem_u32(smem + s * STAGE);
                 const uint32_t b_addr = a_addr + A_BYTES;
@@ -146,85 +203,101 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------ im2col gather of A
-        const int g = threadIdx.x - 64;                  // pixel row in the tile, 0..127
+        // ------------------------------------------------ im2col build of A
+        const int gt = threadIdx.x - 64;                 // 0..255
+        const int g = gt & 127;                          // pixel row in the tile
+        const int h = gt >> 7;                           // which half of the 128-B row
         const int p = p0 + g;
         const bool prow = p < Ho * Wx;
         for (int i = 0; i < niter; ++i) {
-            const int s = i % kTcStages;
-            mbar_wait(&empty[s], ((i / kTcStages) & 1) ^ 1);
+            const int s = i % NS;
             uint8_t *a_s = smem + s * STAGE;
             const int k0 = (kb0 + i) * BK;
-            // each lane decodes the input offset of (BK/32) k values
+            const int ch_lo = k0 / KK;
+            // stage free (non-patch path) / patch landed (patch path; the producer
+            // only loads it after the MMA released the stage)
+            if (kPatch) mbar_wait(&pfull[s], (i / NS) & 1);
+            else mbar_wait(&empty[s], ((i / NS) & 1) ^ 1);
+            // each lane decodes the source offset of BK/32 k values
             int koff[BK / 32];
 #pragma unroll
-            for (int h = 0; h < BK / 32; ++h) {
-                const int k = k0 + h * 32 + (int)lane;
+            for (int t = 0; t < BK / 32; ++t) {
+                const int k = k0 + t * 32 + (int)lane;
                 const int ch = k / KK, rem = k - ch * KK, r = rem / K, c = rem - r * K;
-                koff[h] = k < Ktot ? ch * HW + r * Wx + c : -1;
+                if (kPatch)   // + the channel's misalignment inside its 16-B aligned patch
+                    koff[t] = k < Ktot ? (ch - ch_lo) * geo.npp + ((ch * HW) & (16 / Tr::kElem - 1)) +
+                                             r * Wx + c
+                                       : -1;
+                else koff[t] = k < Ktot ? ch * HW + r * Wx + c : -1;
             }
+            // this thread's half row: 16-B chunks [4h, 4h+4) = BK/2 consecutive k
+            uint32_t v[16];
             if constexpr (kTF32) {
-                uint32_t v[32];
+                const float *src = kPatch ? reinterpret_cast<const float *>(a_s + A_BYTES + B_BYTES)
+                                          : reinterpret_cast<const float *>(I);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int off = __shfl_sync(0xffffffffu, koff[0], j);
-                    const int64_t a = (int64_t)p + off;
-                    v[j] = (prow && off >= 0 && a < CHW)
-                               ? __float_as_uint(__ldg(reinterpret_cast<const float *>(I) + a))
-                               : 0u;
+                for (int j = 0; j < 16; ++j) {
+                    const int off = __shfl_sync(0xffffffffu, koff[0], 16 * h + j);
+                    if (kPatch) {
+                        v[j] = off >= 0 ? __float_as_uint(src[off + g]) : 0u;
+                    } else {
+                        const int64_t a = (int64_t)p + off;
+                        v[j] = (prow && off >= 0 && a < CHW) ? __float_as_uint(__ldg(src + a)) : 0u;
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<uint4 *>(a_s + sw128_off(g, q)) =
-                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             } else {
-                const unsigned short *Ib = reinterpret_cast<const unsigned short *>(I);
-                uint32_t v[32];
+                const unsigned short *src =
+                    kPatch ? reinterpret_cast<const unsigned short *>(a_s + A_BYTES + B_BYTES)
+                           : reinterpret_cast<const unsigned short *>(I);
+                const int kh = h ? koff[BK / 32 - 1] : koff[0];   // this half's k offsets
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < 16; ++j) {
                     uint32_t lohi[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const int kl = 2 * j + e;                       // 0..63
-                        const int off = __shfl_sync(0xffffffffu, koff[kl >> 5], kl & 31);
-                        const int64_t a = (int64_t)p + off;
-                        lohi[e] = (prow && off >= 0 && a < CHW) ? (uint32_t)__ldg(Ib + a) : 0u;
+                        const int off = __shfl_sync(0xffffffffu, kh, 2 * j + e);
+                        if (kPatch) {
+                            lohi[e] = off >= 0 ? (uint32_t)src[off + g] : 0u;
+                        } else {
+                            const int64_t a = (int64_t)p + off;
+                            lohi[e] = (prow && off >= 0 && a < CHW) ? (uint32_t)__ldg(src + a) : 0u;
+                        }
                     }
                     v[j] = lohi[0] | (lohi[1] << 16);
                 }
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<uint4 *>(a_s + sw128_off(g, q)) =
-                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<uint4 *>(a_s + sw128_off(g, 4 * h + q)) =
+                    make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             if constexpr (!kTmaB) {
                 // B rows (filters) gathered too when F rows are not 16-B aligned
                 uint8_t *b_s = a_s + A_BYTES;
                 for (int nr = g; nr < BN; nr += 128) {
                     const int m = n0 + nr;
-                    uint32_t v[32];
+                    uint32_t w[16];
                     if constexpr (kTF32) {
                         const float *Fm = reinterpret_cast<const float *>(F) + (int64_t)m * Ktot;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int k = k0 + j;
-                            v[j] = (m < M && k < Ktot) ? __float_as_uint(__ldg(Fm + k)) : 0u;
+                        for (int j = 0; j < 16; ++j) {
+                            const int k = k0 + 16 * h + j;
+                            w[j] = (m < M && k < Ktot) ? __float_as_uint(__ldg(Fm + k)) : 0u;
                         }
                     } else {
                         const unsigned short *Fm =
                             reinterpret_cast<const unsigned short *>(F) + (int64_t)m * Ktot;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int k = k0 + 2 * j;
+                        for (int j = 0; j < 16; ++j) {
+                            const int k = k0 + 32 * h + 2 * j;
                             const uint32_t lo = (m < M && k < Ktot) ? (uint32_t)__ldg(Fm + k) : 0u;
                             const uint32_t hi = (m < M && k + 1 < Ktot) ? (uint32_t)__ldg(Fm + k + 1) : 0u;
-                            v[j] = lo | (hi << 16);
+                            w[j] = lo | (hi << 16);
                         }
                     }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        *reinterpret_cast<uint4 *>(b_s + sw128_off(nr, q)) =
-                            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    for (int q = 0; q < 4; ++q)
+                        *reinterpret_cast<uint4 *>(b_s + sw128_off(nr, 4 * h + q)) =
+                            make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
                 }
             }
             fence_proxy_async_smem();        // generic-proxy stores -> visible to tcgen05
@@ -234,6 +307,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
 
         // ------------------------------------------------ epilogue
         const int q = (int)(warp & 3);                   // TMEM lane quarter of this warp
+        const int half = (int)(warp - 2) >> 2;           // which half of the BN columns
         const int row = q * 32 + (int)lane;              // pixel row == TMEM lane
         const int pe = p0 + row;
         const int y = pe / Wx, x = pe - y * Wx;
@@ -245,8 +319,8 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const void *__restrict__ 
             mbar_wait(tmem_full, 0);
             tc_fence_after();
         }
-#pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {
+        constexpr int NCB = BN / 32;                     // 32-column blocks
+        for (int cb = half; cb < NCB; cb += 2) {
             uint32_t r[32];
             if (niter > 0) {
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
@@ -329,7 +403,10 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     const int nft = (M + BN - 1) / BN;
     const int tiles = npt * nft;
     int S = 1;
-    while (S < kTcMaxSplit && tiles * S * 2 <= 2 * kNumSMs && 2 * S <= nkb && tiles * S < kNumSMs) S *= 2;
+    while (S < kTcMaxSplit && tiles * S < kNumSMs && 2 * S <= nkb) S *= 2;
+    const TcGeom gp = tc_geom(Wx, K, BN, elem, true);
+    const bool patch = gp.stages >= 2;
+    const TcGeom g = patch ? gp : tc_geom(Wx, K, BN, elem, false);
     p->kernel = 2;
     p->grid_x = S;
     p->grid_y = npt;
@@ -338,17 +415,18 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     p->cluster_x = S;
     p->tile_m = BN;
     p->tile_n = kTcBM;
-    p->smem_bytes = tc_smem_bytes(BN);
+    p->smem_bytes = g.smem;
     const bool aligned = ((Ktot * elem) % 16 == 0) &&
                          (F == nullptr || (reinterpret_cast<uintptr_t>(F) % 16) == 0);
-    p->tma_f = aligned ? 1 : 0;
+    p->tma_f = (aligned ? 1 : 0) | (patch ? 2 : 0);    // bit 0: F by TMA, bit 1: I patch by TMA
     return 0;
 }
 
-template <bool kTF32, int BN, bool kTmaB>
-static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tm, const void *I, int C, int Wx,
-                             int Wy, const void *F, int K, int M, float *O, cudaStream_t s) {
-    auto kern = kmtc_kernel<kTF32, BN, kTmaB>;
+template <bool kTF32, int BN, bool kTmaB, bool kPatch>
+static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CUtensorMap &ti,
+                             const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
+                             float *O, cudaStream_t s) {
+    auto kern = kmtc_kernel<kTF32, BN, kTmaB, kPatch>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return e;
@@ -369,31 +447,52 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tm, const vo
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, tm, I, F, C, Wx, Wy, K, M, O, kb_per_split);
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split);
 }
 
 template <bool kTF32, int BN>
 static cudaError_t launch_tc_bn(const conv_plan &p, const void *I, int C, int Wx, int Wy,
                                 const void *F, int K, int M, float *O, cudaStream_t s) {
-    CUtensorMap tm;
-    memset(&tm, 0, sizeof(tm));
-    if (p.tma_f) {
-        auto encode = get_encode();
-        if (!encode) return cudaErrorNotSupported;
-        const int elem = kTF32 ? 4 : 2;
+    const int elem = kTF32 ? 4 : 2;
+    const CUtensorMapDataType dt =
+        kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap tf, ti;
+    memset(&tf, 0, sizeof(tf));
+    memset(&ti, 0, sizeof(ti));
+    const bool tma_b = (p.tma_f & 1) != 0;
+    bool patch = (p.tma_f & 2) != 0 && (reinterpret_cast<uintptr_t>(I) % 16) == 0;
+    auto encode = get_encode();
+    if ((tma_b || patch) && !encode) return cudaErrorNotSupported;
+    if (tma_b) {
         const cuuint64_t Ktot = (cuuint64_t)C * K * K;
         cuuint64_t dims[2] = {Ktot, (cuuint64_t)M};
         cuuint64_t strides[1] = {Ktot * elem};
         cuuint32_t box[2] = {(cuuint32_t)(128 / elem), (cuuint32_t)BN};
         cuuint32_t estr[2] = {1, 1};
-        CUresult r = encode(&tm, kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                            2, const_cast<void *>(F), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-        return launch_tc<kTF32, BN, true>(p, tm, I, C, Wx, Wy, F, K, M, O, s);
+        if (encode(&tf, dt, 2, const_cast<void *>(F), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
     }
-    return launch_tc<kTF32, BN, false>(p, tm, I, C, Wx, Wy, F, K, M, O, s);
+    if (patch) {
+        const TcGeom g = tc_geom(Wx, K, BN, elem, true);
+        cuuint64_t dims[1] = {(cuuint64_t)C * Wx * Wy};
+        cuuint64_t strides[1] = {0};
+        cuuint32_t box[1] = {(cuuint32_t)g.pb};
+        cuuint32_t estr[1] = {1};
+        if (encode(&ti, dt, 1, const_cast<void *>(I), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            patch = false;
+    }
+    conv_plan q = p;
+    if (!patch) {
+        q.smem_bytes = tc_geom(Wx, K, BN, elem, false).smem;
+        return tma_b ? launch_tc<kTF32, BN, true, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s)
+                     : launch_tc<kTF32, BN, false, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s);
+    }
+    return tma_b ? launch_tc<kTF32, BN, true, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s)
+                 : launch_tc<kTF32, BN, false, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s);
 }
 
 template <bool kTF32>
