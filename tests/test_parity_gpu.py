@@ -235,3 +235,19 @@ def test_output_untouched_on_argument_error(conv):
         conv.conv_single_ex(I, 8, 8, F, 9, 4, O)
     torch.cuda.synchronize()
     assert torch.all(O == 7.0)
+
+
+def test_sharded_multi_virtual_ranks(conv):
+    """sharded_multi on 4 virtual ranks of one GPU concatenates to the full result."""
+    from paper_2212_00404_b200.shard import sharded_multi
+    c = synth.MULTI_LAYERS[2]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=9)
+    Oo, A = oracle.conv_multi(I, F)
+    for prec in ("fp32", "tf32", "bf16"):
+        dt = torch.bfloat16 if prec == "bf16" else torch.float32
+        Id = torch.from_numpy(I).cuda().to(dt)
+        Fd = torch.from_numpy(F).cuda().to(dt)
+        parts = [sharded_multi(Id, Fd, prec, world=4, rank=r) for r in range(4)]
+        torch.cuda.synchronize()
+        Og = torch.cat(parts).cpu().numpy().astype(np.float64)
+        assert_parity(Og, Oo, A, TAU[prec], f"virtual shards {prec}")
