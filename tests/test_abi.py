@@ -95,11 +95,12 @@ def test_plans_cover_every_config_with_one_launch():
         for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
             p = conv.plan_multi(cfg["C"], cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"], prec)
             assert p["kernel"] == kern
-            assert p["cluster_x"] in (1, 2, 4, 8) and p["grid_x"] == p["cluster_x"]
+            assert p["cluster_x"] in (1, 2, 4, 8, 16) and p["grid_x"] == p["cluster_x"]
             assert p["smem_bytes"] <= 227 * 1024
             Ho = cfg["Wy"] - cfg["K"] + 1
             assert p["grid_y"] * p["tile_n"] >= Ho * cfg["Wx"]      # wide pixels covered
             assert p["grid_z"] * p["tile_m"] >= cfg["M"]
             if prec != "fp32":
                 aligned = (cfg["C"] * cfg["K"] ** 2 * (2 if prec == "bf16" else 4)) % 16 == 0
-                assert p["tma_f"] == int(aligned)
+                assert (p["tma_f"] & 1) == int(aligned)        # bit 0: F tiles by TMA
+                assert p["tma_f"] & 2                            # bit 1: I patch by TMA
