@@ -4,37 +4,36 @@
 //
 //   O[m][y][x] = sum_{ch,r,c} I[ch][y+r][x+c] * F[m][ch][r][c]
 //
-// Design:
-//  * Output tile = BM filters x BN "wide" pixels.  A wide pixel p = y*Wx + x
-//    runs over the full input width (x in [0, Wx)); columns x >= Wo are
-//    computed and discarded.  With that indexing the input patch a tile needs
-//    for one channel is ONE contiguous range I[ch][p0 .. p0+BN+(K-1)*Wx+K-1),
-//    so staging is a plain 1-D copy for any alignment.
-//  * The reduction runs over channel chunks of CB channels (the paper's
-//    "segment along ch" of S bytes per filter, with S = CB*K*K*4 B),
-//    double-buffered with cp.async (the paper's prefetch rounds).
-//  * F chunks are stored transposed in smem (k-major, m contiguous) so each
-//    thread reads its 8 filters with two 16-B loads; each thread owns an 8x8
-//    register tile (8 filters x 8 pixels strided by BN/8 -> conflict-free).
+// Design: an implicit GEMM on the FP32 pipes,
+//   D[m][n] = sum_k F[m][k] * B[k][n],  k = (ch, r, c),  n = output pixel y*Wo+x
+//  * CTA tile = BM filters x BN output pixels (compact indexing: no garbage
+//    columns), 256 threads, 8 x 8 register tile per thread taken as two 4-wide
+//    halves in m and in n so every operand load is a 16-B shared load.
+//  * The reduction runs over channel chunks of CB channels — the paper's
+//    segment of S = CB*K*K*4 bytes per filter — double buffered
+//    (the paper's prefetch rounds):
+//      F: 16-B cp.async of the rows as stored into a raw buffer, then an
+//         in-smem transpose to [k][m];
+//      B: the im2col tile [k][n] gathered straight from global/L2 by 4-B
+//         cp.async (one pixel per lane: coalesced), offsets from a small
+//         per-chunk k -> (ch, r, c) table in shared memory.
 //  * Small layers cannot fill 148 SMs with output tiles, so the channel sum is
-//    split across a thread-block cluster of S CTAs (the paper's rejected
-//    Fig. 2(b) split along ch): partial tiles are reduced through
-//    distributed shared memory in fixed rank order (deterministic, no global
-//    atomics, O written once) instead of through global memory.
+//    split across a thread-block cluster of up to 16 CTAs (the paper's
+//    rejected Fig. 2(b) split along ch): partial tiles are reduced
+//    through distributed shared memory in fixed rank order (deterministic, no
+//    global atomics, O written once).
 #include <cstdint>
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace b200 {
 
-
 constexpr int kSimtThreads = 256;              // (BM/8) x (BN/8) threads, 8x8 outputs each
 constexpr int kSimtMaxSplit = 16;              // non-portable cluster size on B200
-constexpr int kSimtStageBudget = 48 * 1024;    // bytes per pipeline stage
-constexpr int kSimtMaxSmem = 200 * 1024;
+constexpr int kSimtMaxSmem = 110 * 1024;       // 2 CTAs per SM
 
-// Fallback for shapes whose staged patch exceeds shared memory (very large K,
-// e.g. K = Wx = Wy): one thread per output, loads through L1, same sum order.
+// Fallback for shapes whose chunk does not fit in shared memory (huge K):
+// one thread per output, loads through L1.
 __global__ void __launch_bounds__(256)
 kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F, int K,
            int M, float *__restrict__ O) {
@@ -58,30 +57,31 @@ kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     }
 }
 
-// KT = compile-time K (1..7) or 0 for a runtime K; CB = channels per stage.
-template <int KT, int BM, int BN>
+// smem layout (floats): F_s[CK][BM] | B_s[2][CK][BN] | Fraw[BM][RS] | koff[CK] (int)
+// (F is double buffered through Fraw: chunk c+1 lands in Fraw while chunk c
+// computes from F_s, and is transposed into F_s once every thread is done.)
+__host__ __device__ constexpr int simt_rs(int CK) { return ((CK - 4 + 31) / 32) * 32 + 4; }
+
+template <int BM, int BN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
-           int Krt, int M, float *__restrict__ O, int ch_per_split, int NP, int CB) {
+           int K, int M, float *__restrict__ O, int ch_per_split, int CB) {
     static_assert((BM / 8) * (BN / 8) == kSimtThreads, "tile must map to 256 threads");
-    constexpr int NT = (BM / 8) * (BN / 8);
-    constexpr int TNS = BN / 8;                     // pixel stride inside a thread tile
-    constexpr int FS = BM + 4;                      // transposed-F row stride (floats)
-    const int K = KT > 0 ? KT : Krt;
+    constexpr int NT = kSimtThreads;
+    constexpr int TNG = BN / 8;                     // thread columns
     const int KK = K * K;
     const int Ho = Wy - K + 1, Wo = Wx - K + 1;
     const int HW = Wx * Wy;
+    const int HoWo = Ho * Wo;
     const int Ktot = C * KK;
+    const int CK = CB * KK;
+    const int RS = simt_rs(CK);
 
     extern __shared__ __align__(16) float smem[];
-    // smem: F_s[2][CB*KK][FS] (transposed, m contiguous) | I_s[2][CB][NP] | Fraw[BM][RS]
-    const int CK = CB * KK;
-    const int RS = ((CK - 4 + 31) / 32) * 32 + 4;   // raw row stride, == 4 (mod 32)
-    const int f_floats = CK * FS;
-    const int i_floats = CB * NP;
-    float *Fs_buf = smem;
-    float *Is_buf = smem + 2 * f_floats;
-    float *Fraw = Is_buf + 2 * i_floats;
+    float *Fs_buf = smem;                           // [CK][BM]
+    float *Bs_buf = smem + CK * BM;                 // [2][CK][BN]
+    float *Fraw = Bs_buf + 2 * CK * BN;             // [BM][RS]
+    int *koff = reinterpret_cast<int *>(Fraw + BM * RS);   // [CK]
 
     const int S = gridDim.x;                        // cluster size == split
     const int split = blockIdx.x;
@@ -91,48 +91,72 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int ch_end = min(C, ch_begin + ch_per_split);
     const int nchunks = ch_end > ch_begin ? (ch_end - ch_begin + CB - 1) / CB : 0;
     const int tid = threadIdx.x;
-    const int tn = tid % TNS, tm = tid / TNS;
-    // 16-B copies of F rows when every row start of every chunk is 16-B aligned
-    const bool vec_f = ((Ktot & 3) == 0) && ((CK & 3) == 0) && ((ch_per_split * KK & 3) == 0) &&
-                       ((reinterpret_cast<uintptr_t>(F) & 15) == 0);
+    const int tn = tid % TNG, tm = tid / TNG;
+    // widest copy of F rows (16, 8 or 4 B) that keeps every row start of every
+    // chunk aligned
+    auto fits = [&](int w) {
+        return (Ktot % w) == 0 && (CK % w) == 0 && ((ch_per_split * KK) % w) == 0 &&
+               (reinterpret_cast<uintptr_t>(F) % (4 * w)) == 0;
+    };
+    const int vw = fits(4) ? 4 : (fits(2) ? 2 : 1);
 
-    // F rows (row-major, as stored) -> Fraw with coalesced cp.async over the flat
-    // (row, 16-B vector) space: every lane busy, one division per copy
+    // k -> input offset within a chunk (channel relative to the chunk start)
+    for (int k = tid; k < CK; k += NT) {
+        const int ch = k / KK, rem = k - ch * KK, r = rem / K;
+        koff[k] = ch * HW + r * Wx + (rem - r * K);
+    }
+    // this thread's im2col pixel (fixed for the whole kernel) and k-lane
+    constexpr int KL = NT / BN > 0 ? NT / BN : 1;
+    const int bn = tid % BN, bkl = tid / BN;
+    const int bo = p0 + bn;
+    const bool bvalid = bo < HoWo;
+    const int by = bvalid ? bo / Wo : 0;
+    const int bbase = by * Wx + (bvalid ? bo - by * Wo : 0);
+
     auto load_f = [&](int chunk) {
         const int ch0 = ch_begin + chunk * CB;
         const int nk = min(CB, ch_end - ch0) * KK;            // valid k of this chunk
         const float *fbase = F + (int64_t)m0 * Ktot + (int64_t)ch0 * KK;
-        if (vec_f) {
-            const int nv = CK >> 2;
-            for (int idx = tid; idx < BM * nv; idx += NT) {
-                const int m = idx / nv, v = idx - m * nv;
-                const bool ok = (m0 + m < M) && 4 * v < nk;      // nk is a multiple of 4 here
-                const float *src = ok ? fbase + (int64_t)m * Ktot + 4 * v : F;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
-                             ::"r"(smem_u32(Fraw + m * RS + 4 * v)), "l"(src), "r"(ok ? 16 : 0)
-                             : "memory");
-            }
-        } else {
-            for (int idx = tid; idx < BM * CK; idx += NT) {
-                const int m = idx / CK, kk = idx - m * CK;
-                const bool ok = (m0 + m < M) && kk < nk;
-                cp_async4(Fraw + m * RS + kk, ok ? fbase + (int64_t)m * Ktot + kk : F, ok);
+        // thread -> fixed vector column v of rows mr, mr + rpt, ...: no division in the loop
+        const int nv = CK / vw;
+        const int rpt = NT / nv;
+        if (tid < nv * rpt) {
+            const int v = tid % nv, mr = tid / nv;
+            const bool kok = vw * v < nk;                     // nk is a multiple of vw
+            const float *src = fbase + (int64_t)mr * Ktot + vw * v;
+            uint32_t dst = smem_u32(Fraw + mr * RS + vw * v);
+            for (int m = mr; m < BM; m += rpt) {
+                const bool ok = kok && (m0 + m < M);
+                const float *sp = ok ? src : F;
+                if (vw == 4)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                                 ::"r"(dst), "l"(sp), "r"(ok ? 16 : 0) : "memory");
+                else if (vw == 2)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                                 ::"r"(dst), "l"(sp), "r"(ok ? 8 : 0) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                                 ::"r"(dst), "l"(sp), "r"(ok ? 4 : 0) : "memory");
+                src += (int64_t)rpt * Ktot;
+                dst += rpt * RS * 4;
             }
         }
     };
-    auto load_i = [&](int chunk, int b) {
+    // im2col tile B[k][n] = I[ch0 + ch][y_n + r][x_n + c] (zero past the valid range)
+    auto load_b = [&](int chunk, int b) {
         const int ch0 = ch_begin + chunk * CB;
-        float *is = Is_buf + b * i_floats;
-        for (int idx = tid; idx < CB * NP; idx += NT) {
-            const int ch = idx / NP, q = idx - ch * NP;
-            const bool ok = (ch0 + ch < ch_end) && (p0 + q < HW);
-            cp_async4(is + idx, ok ? I + (int64_t)(ch0 + ch) * HW + p0 + q : I, ok);
+        const int nk = min(CB, ch_end - ch0) * KK;
+        const float *src = I + (int64_t)ch0 * HW + bbase;
+        float *dst = Bs_buf + b * CK * BN + bn;
+        for (int k = bkl; k < CK; k += KL) {
+            const bool ok = bvalid && k < nk;
+            cp_async4(dst + k * BN, ok ? src + koff[k] : I, ok);
         }
     };
     // Fraw[m][k..k+3] (16-B loads along m: RS == 4 mod 32 -> conflict-free)
     //   -> F_s[k+i][m] (scalar stores, consecutive m -> conflict-free)
-    auto transpose_f = [&](int b) {
-        float *fs = Fs_buf + b * f_floats;
+    auto transpose_f = [&]() {
+        float *fs = Fs_buf;
         const int nq = (CK + 3) / 4;
         for (int u = tid; u < BM * nq; u += NT) {
             const int m = u % BM, q = u / BM;
@@ -140,7 +164,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
             const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                if (4 * q + i < CK) fs[(4 * q + i) * FS + m] = vv[i];
+                if (4 * q + i < CK) fs[(4 * q + i) * BM + m] = vv[i];
         }
     };
 
@@ -152,54 +176,41 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
 
     pdl_wait();
     pdl_trigger();
-    // pipeline: F of chunk c+1 lands in Fraw and I of chunk c+1 in I_s[(c+1)&1]
-    // while chunk c computes; then Fraw is transposed into F_s[(c+1)&1]
+    __syncthreads();                                // koff table
     if (nchunks > 0) {
         load_f(0);
-        load_i(0, 0);
+        load_b(0, 0);
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
-        transpose_f(0);
+        transpose_f();
         __syncthreads();
-        if (nchunks > 1) { load_f(1); load_i(1, 1); }
+        if (nchunks > 1) { load_f(1); load_b(1, 1); }
         cp_async_commit();
     }
     for (int chunk = 0; chunk < nchunks; ++chunk) {
         const int b = chunk & 1;
-        const float *Fs = Fs_buf + b * f_floats;
-        const float *Is = Is_buf + b * i_floats;
-#pragma unroll 1
-        for (int ch = 0; ch < CB; ++ch) {
+        const float *Fs = Fs_buf + tm * 4;
+        const float *Bs = Bs_buf + b * CK * BN + tn * 4;
+#pragma unroll 4
+        for (int k = 0; k < CK; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(Fs + k * BM);
+            const float4 a1 = *reinterpret_cast<const float4 *>(Fs + k * BM + BM / 2);
+            const float4 b0 = *reinterpret_cast<const float4 *>(Bs + k * BN);
+            const float4 b1 = *reinterpret_cast<const float4 *>(Bs + k * BN + BN / 2);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-            for (int r = 0; r < (KT > 0 ? KT : 1); ++r) {
-                for (int rr = (KT > 0 ? r : 0); rr < (KT > 0 ? r + 1 : K); ++rr) {
-                    const float *ip = Is + ch * NP + rr * Wx + tn;
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int c = 0; c < (KT > 0 ? KT : 1); ++c) {
-                        for (int cc = (KT > 0 ? c : 0); cc < (KT > 0 ? c + 1 : K); ++cc) {
-                            float bv[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) bv[j] = ip[cc + j * TNS];
-                            const float *fp = Fs + ((ch * K + rr) * K + cc) * FS + tm * 8;
-                            const float4 a0 = *reinterpret_cast<const float4 *>(fp);
-                            const float4 a1 = *reinterpret_cast<const float4 *>(fp + 4);
-                            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-                        }
-                    }
-                }
-            }
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
         if (chunk + 1 < nchunks) {
             cp_async_wait<0>();                     // chunk c+1 staged
             __syncthreads();                        // ... and everyone is done with chunk c
-            transpose_f(b ^ 1);
+            transpose_f();
             __syncthreads();
-            if (chunk + 2 < nchunks) { load_f(chunk + 2); load_i(chunk + 2, b); }
+            if (chunk + 2 < nchunks) { load_f(chunk + 2); load_b(chunk + 2, b); }
             cp_async_commit();
         }
     }
@@ -207,27 +218,30 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     __syncthreads();
 
     // ---- partial tile -> own smem, then fixed-order (DSMEM) reduction ------
-    float *P = smem;                                // BM x BN
+    float *P = smem;                                // [BM][BN]
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) P[(tm * 8 + i) * BN + tn + j * TNS] = acc[i][j];
+    for (int i = 0; i < 8; ++i) {
+        const int m = (i < 4) ? tm * 4 + i : BM / 2 + tm * 4 + (i - 4);
+        *reinterpret_cast<float4 *>(P + m * BN + tn * 4) =
+            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        *reinterpret_cast<float4 *>(P + m * BN + BN / 2 + tn * 4) =
+            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
     if (S > 1) cluster_sync_all(); else __syncthreads();
 
     const int rows = BM / S;
     const int mlo = split * rows;
     const uint32_t Pbase = smem_u32(P);
+    const int nvalid = min(BN, HoWo - p0);
     for (int idx = tid; idx < rows * BN; idx += NT) {
         const int m = mlo + idx / BN, n = idx % BN;
-        const int p = p0 + n;
-        const int y = p / Wx, x = p - y * Wx;
         float v = 0.f;
         if (S > 1) {
             for (int t = 0; t < S; ++t) v += ld_dsmem_f32(mapa_shared(Pbase + (m * BN + n) * 4, t));
         } else {
             v = P[m * BN + n];
         }
-        if (m0 + m < M && y < Ho && x < Wo) O[(int64_t)(m0 + m) * Ho * Wo + (int64_t)y * Wo + x] = v;
+        if (m0 + m < M && n < nvalid) O[(int64_t)(m0 + m) * HoWo + p0 + n] = v;   // compact: coalesced
     }
     if (S > 1) cluster_sync_all();
 }
@@ -236,36 +250,33 @@ namespace {
 struct SimtTile { int BM, BN; };
 constexpr SimtTile kSimtTiles[3] = {{128, 128}, {64, 256}, {256, 64}};
 
-int simt_np(int BN, int Wx, int K) { return (BN + (K - 1) * Wx + (K - 1) + 3) & ~3; }
-// channels per stage: a multiple of 4 (16-B F rows) within the stage budget
-int simt_cb_for(int BM, int BN, int Wx, int K, int C) {
-    const int per_ch = (K * K * (2 * BM + 5) + 2 * simt_np(BN, Wx, K)) * 4;
-    int cb = (2 * kSimtStageBudget / per_ch) & ~3;
-    if (cb > 8) cb = 8;
-    if (cb < 4) cb = 4;
+int simt_smem(int BM, int BN, int CK) {
+    const int bytes = (CK * BM + 2 * CK * BN + BM * simt_rs(CK)) * 4 + CK * 4;
+    const int pbytes = BM * BN * 4;
+    return bytes > pbytes ? bytes : pbytes;
+}
+// channels per stage: a multiple of 4 (16-B F rows) that fits the smem budget
+int simt_cb_for(int BM, int BN, int K, int C) {
+    int cb = (64 / (K * K) + 3) & ~3;               // ~64 k-steps per chunk
+    if (cb < 8) cb = 8;
+    while (cb > 4 && simt_smem(BM, BN, cb * K * K) > kSimtMaxSmem) cb -= 4;
+    while (cb > 1 && simt_smem(BM, BN, cb * K * K) > kSimtMaxSmem + 16 * 1024) --cb;
     if (cb > C) cb = C;
     return cb < 1 ? 1 : cb;
 }
 // channels per split, a multiple of CB (chunk starts stay 16-B aligned in F)
-void simt_split(int C, int S, int BM, int BN, int Wx, int K, int *CB, int *cps) {
+void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
     int per = (C + S - 1) / S;
-    int cb = simt_cb_for(BM, BN, Wx, K, C);
+    int cb = simt_cb_for(BM, BN, K, C);
     if (cb > per) cb = per >= 4 ? (per & ~3) : per;
     *CB = cb;
     *cps = ((per + cb - 1) / cb) * cb;
 }
-int simt_smem(int BM, int BN, int Wx, int K, int CB) {
-    const int CK = CB * K * K;
-    const int RS = ((CK - 4 + 31) / 32) * 32 + 4;
-    const int bytes = (2 * CK * (BM + 4) + 2 * CB * simt_np(BN, Wx, K) + BM * RS) * 4;
-    const int pbytes = BM * BN * 4;
-    return bytes > pbytes ? bytes : pbytes;
-}
 }  // namespace
 
 int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
-    const int Ho = Wy - K + 1;
-    const int64_t px = (int64_t)Ho * Wx;                  // wide pixels
+    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int64_t px = (int64_t)Ho * Wo;                  // compact output pixels
     // tile shape with the least padded work (ties: the first, 128 x 128)
     int best = 0;
     int64_t best_pad = -1;
@@ -275,10 +286,9 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
         if (best_pad < 0 || pad < best_pad) { best_pad = pad; best = i; }
     }
     const int BM = kSimtTiles[best].BM, BN = kSimtTiles[best].BN;
-    const int CB = simt_cb_for(BM, BN, Wx, K, C);
-    const int smem = simt_smem(BM, BN, Wx, K, CB);
-    if (smem > kSimtMaxSmem) {                           // naive fallback (huge K * Wx)
-        const int64_t n = (int64_t)M * Ho * (Wx - K + 1);
+    const int CB = simt_cb_for(BM, BN, K, C);
+    if (simt_smem(BM, BN, CB * K * K) > kSimtMaxSmem + 64 * 1024) {   // naive fallback (huge K)
+        const int64_t n = (int64_t)M * px;
         int64_t blocks = (n + 255) / 256;
         p->kernel = 1;
         p->grid_x = (int)(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
@@ -304,15 +314,15 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
     p->cluster_x = S;
     p->tile_m = BM;
     p->tile_n = BN;
-    p->smem_bytes = smem;
+    p->smem_bytes = simt_smem(BM, BN, CB * K * K);
     p->tma_f = 0;
     return 0;
 }
 
-template <int KT, int BM, int BN>
+template <int BM, int BN>
 static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx, int Wy,
                               const float *F, int K, int M, float *O, cudaStream_t s) {
-    auto kern = kms_kernel<KT, BM, BN>;
+    auto kern = kms_kernel<BM, BN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return e;
@@ -321,8 +331,7 @@ static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx,
         if (e != cudaSuccess) return e;
     }
     int CB, ch_per_split;
-    simt_split(C, p.cluster_x, BM, BN, Wx, K, &CB, &ch_per_split);
-    const int NP = simt_np(BN, Wx, K);
+    simt_split(C, p.cluster_x, BM, BN, K, &CB, &ch_per_split);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
     cfg.blockDim = dim3(p.block_x);
@@ -337,15 +346,7 @@ static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx,
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, ch_per_split, NP, CB);
-}
-
-template <int KT>
-static cudaError_t launch_kms_tile(const conv_plan &p, const float *I, int C, int Wx, int Wy,
-                                   const float *F, int K, int M, float *O, cudaStream_t s) {
-    if (p.tile_m == 64) return launch_kms<KT, 64, 256>(p, I, C, Wx, Wy, F, K, M, O, s);
-    if (p.tile_m == 256) return launch_kms<KT, 256, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
-    return launch_kms<KT, 128, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
+    return cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, ch_per_split, CB);
 }
 
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
@@ -356,13 +357,9 @@ cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float
         kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I, C, Wx, Wy, F, K, M, O);
         return cudaGetLastError();
     }
-    switch (K) {
-        case 1: return launch_kms_tile<1>(p, I, C, Wx, Wy, F, K, M, O, s);
-        case 3: return launch_kms_tile<3>(p, I, C, Wx, Wy, F, K, M, O, s);
-        case 5: return launch_kms_tile<5>(p, I, C, Wx, Wy, F, K, M, O, s);
-        case 7: return launch_kms_tile<7>(p, I, C, Wx, Wy, F, K, M, O, s);
-        default: return launch_kms_tile<0>(p, I, C, Wx, Wy, F, K, M, O, s);
-    }
+    if (p.tile_m == 64) return launch_kms<64, 256>(p, I, C, Wx, Wy, F, K, M, O, s);
+    if (p.tile_m == 256) return launch_kms<256, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
+    return launch_kms<128, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
 }
 
 }  // namespace b200

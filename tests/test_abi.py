@@ -97,8 +97,9 @@ def test_plans_cover_every_config_with_one_launch():
             assert p["kernel"] == kern
             assert p["cluster_x"] in (1, 2, 4, 8, 16) and p["grid_x"] == p["cluster_x"]
             assert p["smem_bytes"] <= 227 * 1024
-            Ho = cfg["Wy"] - cfg["K"] + 1
-            assert p["grid_y"] * p["tile_n"] >= Ho * cfg["Wx"]      # wide pixels covered
+            Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
+            px = Ho * (Wo if prec == "fp32" else cfg["Wx"])        # compact (SIMT) / wide (TC)
+            assert p["grid_y"] * p["tile_n"] >= px
             assert p["grid_z"] * p["tile_m"] >= cfg["M"]
             if prec != "fp32":
                 aligned = (cfg["C"] * cfg["K"] ** 2 * (2 if prec == "bf16" else 4)) % 16 == 0
