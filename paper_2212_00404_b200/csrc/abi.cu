@@ -15,6 +15,26 @@ int b200::pdl_enabled() {
     return (e && e[0] == '0') ? 0 : 1;
 }
 
+// co-resident clusters of size S on a B200 (148 SMs, 8 GPCs), measured with
+// cudaOccupancyMaxActiveClusters for our kernels (tools/cluster_occ.py)
+static const int kClusters1[17] = {0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7};
+static const int kClusters2[17] = {0, 296, 148, 93, 71, 56, 45, 37, 33, 30, 26, 21, 21, 17, 14, 14, 14};
+
+int b200::choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_unit,
+                       float t_reduce) {
+    const int *tab = ctas_per_sm >= 2 ? kClusters2 : kClusters1;
+    if (max_split > 16) max_split = 16;
+    if (max_split > units) max_split = units;
+    int best = 1;
+    float best_t = -1.f;
+    for (int S = 1; S <= (max_split < 1 ? 1 : max_split); ++S) {
+        const int waves = (tiles + tab[S] - 1) / tab[S];
+        const float t = waves * ((units + S - 1) / S) * t_unit + (S > 1 ? t_reduce : 0.f);
+        if (best_t < 0.f || t < best_t - 1e-6f) { best_t = t; best = S; }
+    }
+    return best;
+}
+
 namespace {
 
 int check_shape(int C, int Wx, int Wy, int K, int M) {
@@ -200,3 +220,9 @@ const char *conv_status_string(int status) {
 int conv_version(void) { return (1 << 16) | 0; }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ diagnostics
+// Max co-resident clusters for a kernel family at a cluster size (tools only).
+extern "C" B200CONV_API int conv_diag_max_clusters(int kernel, int cluster, int smem_bytes) {
+    return kernel == 2 ? tc_max_clusters(cluster, smem_bytes) : simt_max_clusters(cluster, smem_bytes);
+}

@@ -229,8 +229,8 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     }
     if (S > 1) cluster_sync_all(); else __syncthreads();
 
-    const int rows = BM / S;
-    const int mlo = split * rows;
+    const int mlo = split * BM / S;                 // rows [mlo, mhi) reduced by this rank
+    const int rows = (split + 1) * BM / S - mlo;
     const uint32_t Pbase = smem_u32(P);
     const int nvalid = min(BN, HoWo - p0);
     for (int idx = tid; idx < rows * BN; idx += NT) {
@@ -266,9 +266,15 @@ int simt_cb_for(int BM, int BN, int K, int C) {
 }
 // channels per split, a multiple of CB (chunk starts stay 16-B aligned in F)
 void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
-    int per = (C + S - 1) / S;
-    int cb = simt_cb_for(BM, BN, K, C);
-    if (cb > per) cb = per >= 4 ? (per & ~3) : per;
+    const int per = (C + S - 1) / S;
+    const int budget = simt_cb_for(BM, BN, K, C);
+    // largest chunk in {8, 4, 2, 1} (<= budget) that wastes < 1/8 of a split
+    int cb = 1;
+    for (int c : {8, 4, 2}) {
+        if (c > budget || c > per) continue;
+        const int waste = ((per + c - 1) / c) * c - per;
+        if (8 * waste <= per) { cb = c; break; }
+    }
     *CB = cb;
     *cps = ((per + cb - 1) / cb) * cb;
 }
@@ -304,8 +310,11 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
     const int npt = (int)((px + BN - 1) / BN);
     const int nmt = (M + BM - 1) / BM;
     const int tiles = npt * nmt;
-    int S = 1;        // split the channel sum over a cluster until ~2 CTAs per SM
-    while (S < kSimtMaxSplit && tiles * S < 2 * kNumSMs && 2 * S <= C) S *= 2;
+    // split the channel sum over a cluster (unit = 1 channel of a 16K-output
+    // tile, ~0.6 us per 9 taps; DSMEM reduction ~1 us)
+    const int smem = simt_smem(BM, BN, CB * K * K);
+    const int S = choose_split(tiles, C, kSimtMaxSplit, smem <= 113 * 1024 ? 2 : 1,
+                               0.6f * (float)(K * K) / 9.f, 1.0f);
     p->kernel = 1;
     p->grid_x = S;
     p->grid_y = npt;
@@ -314,7 +323,7 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
     p->cluster_x = S;
     p->tile_m = BM;
     p->tile_n = BN;
-    p->smem_bytes = simt_smem(BM, BN, CB * K * K);
+    p->smem_bytes = smem;
     p->tma_f = 0;
     return 0;
 }
@@ -347,6 +356,26 @@ static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx,
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, ch_per_split, CB);
+}
+
+int simt_max_clusters(int cluster, int smem) {
+    auto kern = kms_kernel<128, 128>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster, 1, 1);
+    cfg.blockDim = dim3(kSimtThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = -1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
+    return n;
 }
 
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,

@@ -42,7 +42,7 @@ namespace b200 {
 
 constexpr int kTcThreads = 320;
 constexpr int kTcBM = 128;            // pixels per tile (UMMA M)
-constexpr int kTcMaxSplit = 8;
+constexpr int kTcMaxSplit = 16;      // non-portable cluster size on B200
 constexpr int kTcSmemMax = 225 * 1024;
 
 template <bool kTF32>
@@ -349,8 +349,8 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     if (S > 1) {
         // ---------------------------------------------- split-K reduce via DSMEM
         cluster_sync_all();
-        const int rows = BN / S;                         // filters owned by this rank
-        const int nlo = split * rows;
+        const int nlo = split * BN / S;                  // filters [nlo, nhi) owned by this rank
+        const int rows = (split + 1) * BN / S - nlo;
         const uint32_t Pbase = smem_u32(smem);
         const int64_t plane = (int64_t)Ho * Wo;
         for (int idx = threadIdx.x; idx < rows * kTcBM; idx += kTcThreads) {
@@ -402,8 +402,10 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     const int npt = (Ho * Wx + kTcBM - 1) / kTcBM;
     const int nft = (M + BN - 1) / BN;
     const int tiles = npt * nft;
-    int S = 1;
-    while (S < kTcMaxSplit && tiles * S < kNumSMs && 2 * S <= nkb) S *= 2;
+    // split the k loop over a cluster (unit = 1 k-block ~0.25 us; prologue +
+    // DSMEM reduction ~2 us), at least 2 k-blocks per split
+    const int S = choose_split(tiles, nkb, nkb / 2 < kTcMaxSplit ? (nkb / 2 > 0 ? nkb / 2 : 1) : kTcMaxSplit,
+                               1, 0.25f, 1.0f);
     const TcGeom gp = tc_geom(Wx, K, BN, elem, true);
     const bool patch = gp.stages >= 2;
     const TcGeom g = patch ? gp : tc_geom(Wx, K, BN, elem, false);
@@ -430,6 +432,10 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return e;
+    if (p.cluster_x > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     const int BK = kTF32 ? 32 : 64;
     const int nkb = (int)(((int64_t)C * K * K + BK - 1) / BK);
     const int kb_per_split = (nkb + p.cluster_x - 1) / p.cluster_x;
@@ -503,6 +509,26 @@ static cudaError_t launch_tc_prec(const conv_plan &p, const void *I, int C, int 
         case 64: return launch_tc_bn<kTF32, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
         default: return launch_tc_bn<kTF32, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
     }
+}
+
+int tc_max_clusters(int cluster, int smem) {
+    auto kern = kmtc_kernel<true, 128, true, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster, 1, 1);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = -1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
+    return n;
 }
 
 cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,

@@ -26,4 +26,16 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
 cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
                             float *O, bool bf16, cudaStream_t s);
 
+// Split-K chooser: cluster size S (1..max_split) minimising
+//   waves(S) * ceil(units / S) * t_unit + (S > 1) * t_reduce,
+// waves(S) = ceil(tiles / clusters_resident(S)), with the co-resident cluster
+// counts MEASURED on B200 (cudaOccupancyMaxActiveClusters; tools/cluster_occ.py)
+// for kernels that fit 1 or 2 CTAs per SM.
+int choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_unit,
+                 float t_reduce);
+
+// max co-resident clusters (diagnostics)
+int tc_max_clusters(int cluster, int smem);
+int simt_max_clusters(int cluster, int smem);
+
 }  // namespace b200

@@ -95,7 +95,7 @@ def test_plans_cover_every_config_with_one_launch():
         for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
             p = conv.plan_multi(cfg["C"], cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"], prec)
             assert p["kernel"] == kern
-            assert p["cluster_x"] in (1, 2, 4, 8, 16) and p["grid_x"] == p["cluster_x"]
+            assert 1 <= p["cluster_x"] <= 16 and p["grid_x"] == p["cluster_x"]
             assert p["smem_bytes"] <= 227 * 1024
             Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
             px = Ho * (Wo if prec == "fp32" else cfg["Wx"])        # compact (SIMT) / wide (TC)
