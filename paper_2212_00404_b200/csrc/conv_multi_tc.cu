@@ -27,10 +27,11 @@
 // tiles through DSMEM in fixed rank order (deterministic, O written once).
 //
 // Warp roles (320 threads):
-//   warp 0      TMA producer: F tile (B) + input patch      [elected lane]
-//   warp 1      TMEM allocator + MMA issuer                  [elected lane]
-//   warps 2..9  im2col build of A (2 threads per pixel row), then epilogue
+//   warps 0..7  im2col build of A (2 threads per pixel row), then epilogue
+//   warp 8      TMA producer: F tile (B) + input patch
+//   warp 9      TMEM allocator + MMA issuer                  [elected lane]
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <cuda_bf16.h>
@@ -40,10 +41,17 @@
 
 namespace b200 {
 
-constexpr int kTcThreads = 320;
+constexpr int kTcProducers = 2;       // producer warps (alternate stages)
+constexpr int kTcThreads = 32 * (8 + kTcProducers + 1);
+// Warp roles.  The SM sub-partition scheduler favours higher warp ids, so the
+// single-thread producer and MMA roles take the two highest ids: spinning
+// im2col warps on the same sub-partition can never starve them.
+constexpr uint32_t kProdWarp = 8;     // TMA producers: warps 8 .. 8+kTcProducers-1
+constexpr uint32_t kMmaWarp = 8 + kTcProducers;   // TMEM allocator + tcgen05.mma issuer
 constexpr int kTcBM = 128;            // pixels per tile (UMMA M)
 constexpr int kTcMaxSplit = 16;      // non-portable cluster size on B200
 constexpr int kTcSmemMax = 225 * 1024;
+constexpr int kTcMaxStages = 8;
 
 template <bool kTF32>
 struct TcTraits {
@@ -62,6 +70,7 @@ struct TcGeom {
     int npp;      // patch stride per channel in smem (elements) = nbox * pb
     int pch;      // max channels touched by one k-block
     int patch_bytes;
+    int tab_bytes;
     int stages;
     int stage_bytes;
     int smem;
@@ -81,9 +90,11 @@ __host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool 
     g.pch = (BK + K * K - 1) / (K * K) + 1;
     g.patch_bytes = patch ? ((g.pch * g.npp * elem + 1023) & ~1023) : 0;
     g.stage_bytes = kTcBM * 128 + BN * 128 + g.patch_bytes;
-    int st = (kTcSmemMax - 1024 - 512) / g.stage_bytes;
-    g.stages = st > 4 ? 4 : st;
-    g.smem = 1024 + g.stages * g.stage_bytes + 512;
+    // k -> patch offset table for every phase (k0 mod K*K) of a k-block (K <= 7)
+    g.tab_bytes = (patch && K <= 7) ? K * K * BK * 4 : 0;
+    int st = (kTcSmemMax - 1024 - 512 - g.tab_bytes) / g.stage_bytes;
+    g.stages = st > kTcMaxStages ? kTcMaxStages : st;
+    g.smem = 1024 + g.stages * g.stage_bytes + 512 + g.tab_bytes;
     return g;
 }
 
@@ -92,11 +103,17 @@ __device__ __forceinline__ uint32_t sw128_off(int g, int j) {
     return (uint32_t)((g >> 3) * 1024 + (g & 7) * 128 + ((j ^ (g & 7)) << 4));
 }
 
+__device__ unsigned long long g_tc_stamps[1024];   // diagnostics (dbg & 128)
+
+int tc_read_stamps(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_tc_stamps, sizeof(g_tc_stamps)) == cudaSuccess ? 0 : 1;
+}
+
 template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 __global__ void __launch_bounds__(kTcThreads, 1)
 kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
             const void *__restrict__ Iv, const void *__restrict__ Fv, int C, int Wx, int Wy,
-            int K, int M, float *__restrict__ O, int kb_per_split) {
+            int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg) {
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
     constexpr int BK = Tr::kBK;
@@ -128,13 +145,29 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);   // A+B ready (MMA)
-    uint64_t *pfull = full + 4;                                          // patch landed
-    uint64_t *empty = pfull + 4;                                         // MMA done with stage
-    uint64_t *tmem_full = empty + 4;
+    uint64_t *pfull = full + kTcMaxStages;                               // patch landed
+    uint64_t *empty = pfull + kTcMaxStages;                              // MMA done with stage
+    uint64_t *tmem_full = empty + kTcMaxStages;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    int *ktab = reinterpret_cast<int *>(smem + NS * STAGE + 512);        // [K*K][BK]
+    const bool use_tab = kPatch && patch2d && geo.tab_bytes > 0;
+    if (use_tab) {
+        for (int idx = threadIdx.x; idx < KK * BK; idx += kTcThreads) {
+            const int u = idx / BK + idx % BK;             // phase + j
+            const int rem = u % KK;
+            ktab[idx] = (u / KK) * geo.npp + (rem / K) * Wx + (rem % K);
+        }
+    }
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    // dbg & 128: CTA (0,0,0) records globaltimer stamps per iteration into O
+    //   O[i] producer issue, O[256+i] gather(warp 2) arrive, O[512+i] MMA commit
+    const bool stamp = (dbg & 128) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    auto gtime = []() { uint64_t t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)); return t; };
+    auto wait = [&](uint64_t *bar, uint32_t par) {
+        if (dbg & 64) mbar_wait_poll(bar, par); else mbar_wait(bar, par);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -147,7 +180,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
         if (kTmaB) tma_prefetch_desc(&tmapF);
         if (kPatch) tma_prefetch_desc(&tmapI);
     }
-    if (warp == 1) tmem_alloc<BN>(tmem_slot);
+    if (warp == kMmaWarp) tmem_alloc<BN>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -155,56 +188,85 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     pdl_wait();                     // prologue above overlaps the previous kernel's tail
     pdl_trigger();
 
-    if (warp == 0) {
+    if (warp >= kProdWarp && warp < kMmaWarp) {
         // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            for (int i = 0; i < niter; ++i) {
-                const int s = i % NS;
-                mbar_wait(&empty[s], ((i / NS) & 1) ^ 1);
-                uint8_t *st = smem + s * STAGE;
-                if (kPatch) {
-                    const int k0 = (kb0 + i) * BK;
-                    const int ch_lo = k0 / KK;
-                    const int ch_hi = min(C - 1, (min(k0 + BK, Ktot) - 1) / KK);
-                    const int nch = ch_hi - ch_lo + 1;
-                    mbar_arrive_expect_tx(&pfull[s], (uint32_t)(nch * geo.npp * Tr::kElem));
-                    T *patch = reinterpret_cast<T *>(st + A_BYTES + B_BYTES);
-                    for (int j = 0; j < nch; ++j) {
-                        const int start = ((ch_lo + j) * HW + p0) & ~(16 / Tr::kElem - 1);
+        // The whole warp runs the loop; lane 0 owns the barriers and the F
+        // tile, lanes 0..nch-1 issue one channel's patch boxes each, so the
+        // per-stage issue latency is not one thread's serial chain.
+        const int ch_mask = 16 / Tr::kElem - 1;
+        const int pw = (int)(warp - kProdWarp);          // this producer takes stages pw, pw+P, ...
+        int k0 = (kb0 + pw) * BK;
+        int ch_lo = k0 / KK;                             // incremental from here on
+        for (int i = pw; i < niter; i += kTcProducers, k0 += kTcProducers * BK) {
+            const int s = i % NS, ph = (i / NS) & 1;
+            if (stamp && lane == 0 && i < 128) g_tc_stamps[768 + i] = gtime();
+            if (lane == 0) wait(&empty[s], ph ^ 1);
+            __syncwarp();
+            if (stamp && lane == 0 && i < 128) g_tc_stamps[896 + i] = gtime();
+            uint8_t *st = smem + s * STAGE;
+            if (kPatch) {
+                while ((ch_lo + 1) * KK <= k0) ++ch_lo;
+                const int k_end = min(k0 + BK, Ktot) - 1;
+                int ch_hi = ch_lo;
+                while ((ch_hi + 1) * KK <= k_end) ++ch_hi;
+                const int nch = ch_hi - ch_lo + 1;
+                if (patch2d) {
+                    // one 2-D box [pch channels][pb pixels] (I viewed as [C][HW])
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&pfull[s], (uint32_t)(geo.pch * geo.pb * Tr::kElem));
+                        tma_load_2d(st + A_BYTES + B_BYTES, &tmapI, &pfull[s], p0, ch_lo);
+                    }
+                } else {
+                    if (lane == 0) {
+                        if (dbg & 8) mbar_arrive(&pfull[s]);
+                        else mbar_arrive_expect_tx(&pfull[s], (uint32_t)(nch * geo.npp * Tr::kElem));
+                    }
+                    __syncwarp();
+                    if (!(dbg & 8) && (int)lane < nch) {
+                        T *patch = reinterpret_cast<T *>(st + A_BYTES + B_BYTES) + lane * geo.npp;
+                        const int start = ((ch_lo + (int)lane) * HW + p0) & ~ch_mask;
                         for (int b = 0; b < geo.nbox; ++b)
-                            tma_load_1d(patch + j * geo.npp + b * geo.pb, &tmapI, &pfull[s],
-                                        start + b * geo.pb);
+                            tma_load_1d(patch + b * geo.pb, &tmapI, &pfull[s], start + b * geo.pb);
                     }
                 }
+            }
+            if (lane == 0) {
+                if (stamp && i < 256) g_tc_stamps[i] = gtime();
                 if (kTmaB) {
-                    mbar_arrive_expect_tx(&full[s], B_BYTES);
-                    tma_load_2d(st + A_BYTES, &tmapF, &full[s], (kb0 + i) * BK, n0);
+                    if (dbg & 2) {
+                        mbar_arrive(&full[s]);
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], B_BYTES);
+                        tma_load_2d(st + A_BYTES, &tmapF, &full[s], k0, n0);
+                    }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
             for (int i = 0; i < niter; ++i) {
                 const int s = i % NS;
-                mbar_wait(&full[s], (i / NS) & 1);
+                wait(&full[s], (i / NS) & 1);
                 tc_fence_after();
                 const uint32_t a_addr = smem_u32(smem + s * STAGE);
                 const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BK / Tr::kUmmaK; ++kk) {
+                    if (dbg & 4) break;
                     umma_ss<kTF32>(tmem, umma_desc_k_sw128(a_addr + kk * 32),
                                    umma_desc_k_sw128(b_addr + kk * 32), IDESC,
                                    (i > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&empty[s]);
+                if (dbg & 16) mbar_arrive(&empty[s]); else umma_commit(&empty[s]);
+                if (stamp && i < 256) g_tc_stamps[512 + i] = gtime();
             }
             umma_commit(tmem_full);       // fires when all MMAs above are complete
         }
         __syncwarp();
     } else {
         // ------------------------------------------------ im2col build of A
-        const int gt = threadIdx.x - 64;                 // 0..255
+        const int gt = threadIdx.x;                      // 0..255 (warps 0..7)
         const int g = gt & 127;                          // pixel row in the tile
         const int h = gt >> 7;                           // which half of the 128-B row
         const int p = p0 + g;
@@ -216,54 +278,86 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
             const int ch_lo = k0 / KK;
             // stage free (non-patch path) / patch landed (patch path; the producer
             // only loads it after the MMA released the stage)
-            if (kPatch) mbar_wait(&pfull[s], (i / NS) & 1);
-            else mbar_wait(&empty[s], ((i / NS) & 1) ^ 1);
-            // each lane decodes the source offset of BK/32 k values
-            int koff[BK / 32];
-#pragma unroll
-            for (int t = 0; t < BK / 32; ++t) {
-                const int k = k0 + t * 32 + (int)lane;
-                const int ch = k / KK, rem = k - ch * KK, r = rem / K, c = rem - r * K;
-                if (kPatch)   // + the channel's misalignment inside its 16-B aligned patch
-                    koff[t] = k < Ktot ? (ch - ch_lo) * geo.npp + ((ch * HW) & (16 / Tr::kElem - 1)) +
-                                             r * Wx + c
-                                       : -1;
-                else koff[t] = k < Ktot ? ch * HW + r * Wx + c : -1;
+            if (kPatch) wait(&pfull[s], (i / NS) & 1);
+            else wait(&empty[s], ((i / NS) & 1) ^ 1);
+            if (dbg & 1) {
+                if (!(dbg & 32)) fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+                if (stamp && warp == 0 && lane == 0 && i < 256) g_tc_stamps[256 + i] = gtime();
+                continue;
             }
-            // this thread's half row: 16-B chunks [4h, 4h+4) = BK/2 consecutive k
             uint32_t v[16];
-            if constexpr (kTF32) {
-                const float *src = kPatch ? reinterpret_cast<const float *>(a_s + A_BYTES + B_BYTES)
-                                          : reinterpret_cast<const float *>(I);
+            if (use_tab && k0 + BK <= Ktot) {
+                // offsets of this thread's BK/2 k values from the phase table (16-B broadcast loads)
+                const int4 *trow = reinterpret_cast<const int4 *>(ktab + (k0 - ch_lo * KK) * BK + (BK / 2) * h);
+                if constexpr (kTF32) {
+                    const float *src = reinterpret_cast<const float *>(a_s + A_BYTES + B_BYTES) + g;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int off = __shfl_sync(0xffffffffu, koff[0], 16 * h + j);
-                    if (kPatch) {
-                        v[j] = off >= 0 ? __float_as_uint(src[off + g]) : 0u;
-                    } else {
-                        const int64_t a = (int64_t)p + off;
-                        v[j] = (prow && off >= 0 && a < CHW) ? __float_as_uint(__ldg(src + a)) : 0u;
+                    for (int q = 0; q < 4; ++q) {
+                        const int4 o = trow[q];
+                        v[4 * q] = __float_as_uint(src[o.x]);
+                        v[4 * q + 1] = __float_as_uint(src[o.y]);
+                        v[4 * q + 2] = __float_as_uint(src[o.z]);
+                        v[4 * q + 3] = __float_as_uint(src[o.w]);
+                    }
+                } else {
+                    const unsigned short *src =
+                        reinterpret_cast<const unsigned short *>(a_s + A_BYTES + B_BYTES) + g;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int4 o = trow[q];
+                        v[2 * q] = (uint32_t)src[o.x] | ((uint32_t)src[o.y] << 16);
+                        v[2 * q + 1] = (uint32_t)src[o.z] | ((uint32_t)src[o.w] << 16);
                     }
                 }
             } else {
-                const unsigned short *src =
-                    kPatch ? reinterpret_cast<const unsigned short *>(a_s + A_BYTES + B_BYTES)
-                           : reinterpret_cast<const unsigned short *>(I);
-                const int kh = h ? koff[BK / 32 - 1] : koff[0];   // this half's k offsets
+                // each lane decodes the source offset of BK/32 k values
+                int koff[BK / 32];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    uint32_t lohi[2];
+                for (int t = 0; t < BK / 32; ++t) {
+                    const int k = k0 + t * 32 + (int)lane;
+                    const int ch = k / KK, rem = k - ch * KK, r = rem / K, c = rem - r * K;
+                    if (kPatch)   // + the channel's misalignment inside its 16-B aligned patch
+                        koff[t] = k < Ktot ? (ch - ch_lo) * geo.npp + ((ch * HW) & (16 / Tr::kElem - 1)) +
+                                                 r * Wx + c
+                                           : -1;
+                    else koff[t] = k < Ktot ? ch * HW + r * Wx + c : -1;
+                }
+                // this thread's half row: 16-B chunks [4h, 4h+4) = BK/2 consecutive k
+                if constexpr (kTF32) {
+                    const float *src = kPatch ? reinterpret_cast<const float *>(a_s + A_BYTES + B_BYTES)
+                                              : reinterpret_cast<const float *>(I);
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int off = __shfl_sync(0xffffffffu, kh, 2 * j + e);
+                    for (int j = 0; j < 16; ++j) {
+                        const int off = __shfl_sync(0xffffffffu, koff[0], 16 * h + j);
                         if (kPatch) {
-                            lohi[e] = off >= 0 ? (uint32_t)src[off + g] : 0u;
+                            v[j] = off >= 0 ? __float_as_uint(src[off + g]) : 0u;
                         } else {
                             const int64_t a = (int64_t)p + off;
-                            lohi[e] = (prow && off >= 0 && a < CHW) ? (uint32_t)__ldg(src + a) : 0u;
+                            v[j] = (prow && off >= 0 && a < CHW) ? __float_as_uint(__ldg(src + a)) : 0u;
                         }
                     }
-                    v[j] = lohi[0] | (lohi[1] << 16);
+                } else {
+                    const unsigned short *src =
+                        kPatch ? reinterpret_cast<const unsigned short *>(a_s + A_BYTES + B_BYTES)
+                               : reinterpret_cast<const unsigned short *>(I);
+                    const int kh = h ? koff[BK / 32 - 1] : koff[0];   // this half's k offsets
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        uint32_t lohi[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int off = __shfl_sync(0xffffffffu, kh, 2 * j + e);
+                            if (kPatch) {
+                                lohi[e] = off >= 0 ? (uint32_t)src[off + g] : 0u;
+                            } else {
+                                const int64_t a = (int64_t)p + off;
+                                lohi[e] = (prow && off >= 0 && a < CHW) ? (uint32_t)__ldg(src + a) : 0u;
+                            }
+                        }
+                        v[j] = lohi[0] | (lohi[1] << 16);
+                    }
                 }
             }
 #pragma unroll
@@ -303,11 +397,12 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
             fence_proxy_async_smem();        // generic-proxy stores -> visible to tcgen05
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
+            if (stamp && warp == 0 && lane == 0 && i < 256) g_tc_stamps[256 + i] = gtime();
         }
 
         // ------------------------------------------------ epilogue
         const int q = (int)(warp & 3);                   // TMEM lane quarter of this warp
-        const int half = (int)(warp - 2) >> 2;           // which half of the BN columns
+        const int half = (int)warp >> 2;                 // which half of the BN columns
         const int row = q * 32 + (int)lane;              // pixel row == TMEM lane
         const int pe = p0 + row;
         const int y = pe / Wx, x = pe - y * Wx;
@@ -353,19 +448,29 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
         const int rows = (split + 1) * BN / S - nlo;
         const uint32_t Pbase = smem_u32(smem);
         const int64_t plane = (int64_t)Ho * Wo;
-        for (int idx = threadIdx.x; idx < rows * kTcBM; idx += kTcThreads) {
-            const int nl = nlo + idx / kTcBM, row = idx % kTcBM;
-            const int pe = p0 + row;
-            const int y = pe / Wx, x = pe - y * Wx;
-            const uint32_t off = (uint32_t)((nl * kTcBM + row) * 4);
-            float v = 0.f;
-            for (int t = 0; t < S; ++t) v += ld_dsmem_f32(mapa_shared(Pbase + off, (uint32_t)t));
+        // 4 pixels per thread: 16-B DSMEM loads from every rank, summed in rank order
+        for (int idx = threadIdx.x; idx < rows * (kTcBM / 4); idx += kTcThreads) {
+            const int nl = nlo + idx / (kTcBM / 4), row0 = 4 * (idx % (kTcBM / 4));
+            const uint32_t off = (uint32_t)((nl * kTcBM + row0) * 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int t = 0; t < S; ++t) {
+                const float4 u = ld_dsmem_f32x4(mapa_shared(Pbase + off, (uint32_t)t));
+                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+            }
             const int m = n0 + nl;
-            if (m < M && pe < Ho * Wx && x < Wo) O[(int64_t)m * plane + (int64_t)y * Wo + x] = v;
+            if (m < M) {
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int pe = p0 + row0 + e;
+                    const int y = pe / Wx, x = pe - y * Wx;
+                    if (pe < Ho * Wx && x < Wo) O[(int64_t)m * plane + (int64_t)y * Wo + x] = vv[e];
+                }
+            }
         }
         cluster_sync_all();
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<BN>(tmem);
     }
@@ -385,9 +490,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+// filters per CTA tile (UMMA N).  N = 256 halves how often one im2col tile is
+// rebuilt (once per filter tile) when there are many filters.
 int tc_bn(int M) {
     if (M <= 32) return 32;
     if (M <= 64) return 64;
+    if (M >= 1024) return 256;
     return 128;
 }
 }  // namespace
@@ -427,7 +535,7 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
 template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CUtensorMap &ti,
                              const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
-                             float *O, cudaStream_t s) {
+                             float *O, int patch2d, cudaStream_t s) {
     auto kern = kmtc_kernel<kTF32, BN, kTmaB, kPatch>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
@@ -453,7 +561,9 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split);
+    const char *dbgs = getenv("B200CONV_TC_DBG");
+    const int dbg = dbgs ? atoi(dbgs) : 0;
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg);
 }
 
 template <bool kTF32, int BN>
@@ -480,25 +590,41 @@ static cudaError_t launch_tc_bn(const conv_plan &p, const void *I, int C, int Wx
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
+    int patch2d = 0;
     if (patch) {
         const TcGeom g = tc_geom(Wx, K, BN, elem, true);
-        cuuint64_t dims[1] = {(cuuint64_t)C * Wx * Wy};
-        cuuint64_t strides[1] = {0};
-        cuuint32_t box[1] = {(cuuint32_t)g.pb};
-        cuuint32_t estr[1] = {1};
-        if (encode(&ti, dt, 1, const_cast<void *>(I), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            patch = false;
+        const int HW = Wx * Wy;
+        // one 2-D box per stage when channel rows are 16-B strided and one box
+        // covers the patch; else one 1-D box per channel (any alignment)
+        if (g.nbox == 1 && ((int64_t)HW * elem) % 16 == 0) {
+            cuuint64_t dims[2] = {(cuuint64_t)HW, (cuuint64_t)C};
+            cuuint64_t strides[1] = {(cuuint64_t)HW * elem};
+            cuuint32_t box[2] = {(cuuint32_t)g.pb, (cuuint32_t)g.pch};
+            cuuint32_t estr[2] = {1, 1};
+            if (encode(&ti, dt, 2, const_cast<void *>(I), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                patch2d = 1;
+        }
+        if (!patch2d) {
+            cuuint64_t dims[1] = {(cuuint64_t)C * HW};
+            cuuint64_t strides[1] = {0};
+            cuuint32_t box[1] = {(cuuint32_t)g.pb};
+            cuuint32_t estr[1] = {1};
+            if (encode(&ti, dt, 1, const_cast<void *>(I), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                patch = false;
+        }
     }
     conv_plan q = p;
     if (!patch) {
         q.smem_bytes = tc_geom(Wx, K, BN, elem, false).smem;
-        return tma_b ? launch_tc<kTF32, BN, true, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s)
-                     : launch_tc<kTF32, BN, false, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s);
+        return tma_b ? launch_tc<kTF32, BN, true, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, patch2d, s)
+                     : launch_tc<kTF32, BN, false, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, patch2d, s);
     }
-    return tma_b ? launch_tc<kTF32, BN, true, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s)
-                 : launch_tc<kTF32, BN, false, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, s);
+    return tma_b ? launch_tc<kTF32, BN, true, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, patch2d, s)
+                 : launch_tc<kTF32, BN, false, true>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, patch2d, s);
 }
 
 template <bool kTF32>
@@ -507,6 +633,7 @@ static cudaError_t launch_tc_prec(const conv_plan &p, const void *I, int C, int 
     switch (p.tile_m) {
         case 32: return launch_tc_bn<kTF32, 32>(p, I, C, Wx, Wy, F, K, M, O, s);
         case 64: return launch_tc_bn<kTF32, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
+        case 256: return launch_tc_bn<kTF32, 256>(p, I, C, Wx, Wy, F, K, M, O, s);
         default: return launch_tc_bn<kTF32, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
     }
 }

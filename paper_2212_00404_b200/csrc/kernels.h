@@ -36,6 +36,7 @@ int choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_u
 
 // max co-resident clusters (diagnostics)
 int tc_max_clusters(int cluster, int smem);
+int tc_read_stamps(unsigned long long *host);
 int simt_max_clusters(int cluster, int smem);
 
 }  // namespace b200
