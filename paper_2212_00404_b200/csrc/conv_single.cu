@@ -232,7 +232,6 @@ ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__re
 }
 
 namespace {
-constexpr int kKsTargetCtas = 4 * kNumSMs;
 constexpr int kKsMaxSmem = 110 * 1024;
 
 // (R filters, RR rows) per lane and item: K=1 store-bound -> more filters;
@@ -257,13 +256,24 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
     const int TX = ks_TX(Wo);
     if (K <= 7 && TX <= 8) {
         const int R = ks_R(K);
-        int TY = Ho < 16 ? Ho : 16;
+        // (band rows TY, filters per CTA m_per): minimise waves x work per CTA on
+        // 148 SMs x 2 CTAs (+ a per-CTA staging cost), i.e. avoid a ragged last wave
+        const int slots = 2 * kNumSMs;
+        int TY = Ho < 16 ? Ho : 16, m_per = R;
+        double best = -1.0;
+        for (int ty : {8, 16}) {
+            const int t = Ho < ty ? Ho : ty;
+            const int nb = (Ho + t - 1) / t;
+            for (int mp = R; mp < M + R; mp += R) {
+                const int ctas = nb * ((M + mp - 1) / mp);
+                const int waves = (ctas + slots - 1) / slots;
+                const double cost = waves * ((double)t * mp + 4.0 * (t + K - 1));
+                if (best < 0 || cost < best - 1e-9) { best = cost; TY = t; m_per = mp; }
+                if (ctas <= slots) break;                 // larger chunks only lengthen the wave
+            }
+            if (Ho <= ty) break;
+        }
         const int bands = (Ho + TY - 1) / TY;
-        const int max_chunks = (M + R - 1) / R;
-        int nmc = (kKsTargetCtas + bands - 1) / bands;
-        nmc = nmc < 1 ? 1 : (nmc > max_chunks ? max_chunks : nmc);
-        int m_per = (M + nmc - 1) / nmc;
-        m_per = ((m_per + R - 1) / R) * R;
         p->kernel = 0;
         p->block_x = kKsThreads;
         p->grid_x = (M + m_per - 1) / m_per;
