@@ -299,7 +299,8 @@ def run_ours(args):
         amount = sum(roof_for(c, pk)[3] for c in cs)
         achieved = amount / (us * 1e-6)
         kernels[f"{key[0]}/{key[1]}"] = {
-            "kernel": key[0], "bound": b, "launches_per_step": len(cs), "us_per_step": round(us, 2),
+            "kernel": key[0], "bound": b, "launches_per_step": len(cs),
+            "kernel_launches_per_step": sum(c["plan"]["launches"] for c in cs), "us_per_step": round(us, 2),
             "avg_launch_us": round(us / len(cs), 3), "share": round(us / step_us_sum, 3),
             "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": unit,
             "frac": round(achieved / peak, 4)}
@@ -309,6 +310,10 @@ def run_ours(args):
                 "frac": d["frac"], "traffic": _traffic_lookup(dom_key),
                 "kernel": dom_key, "share_of_step": d["share"],
                 "launches_per_step": d["launches_per_step"], "avg_launch_us": d["avg_launch_us"],
+                "kernel_launches_per_step": d["kernel_launches_per_step"],
+                "launch_note": "a launch = one call of the hot path; calls whose channel split is reduced "
+                               "through the split-K workspace are 2 kernels (main + fixed-order reduce), "
+                               "both inside the timed duration",
                 "peak_source": pk["source"] + (" x0.5 (tf32 = bf16/2, guide ratio)"
                                                if "tf32" in dom_key and d["bound"] == "tensor" else "")}
 
@@ -345,7 +350,7 @@ def run_ours(args):
         "roofline": roofline,
         "kernels": kernels,
         "layers_b2b": layers,
-        "gpu_launches": len(calls) * args.steps,
+        "gpu_launches": sum(c["plan"]["launches"] for c in calls) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "strong_sweep": strong,

@@ -24,15 +24,20 @@
  *   O : [M][Wy-K+1][Wx-K+1], fully overwritten, never accumulated into.
  *
  * Ownership: every array pointer of the device entry points is a CUDA device
- * pointer owned by the caller (the library allocates nothing and keeps no
- * pointer after the call).  The *_host entry points take host pointers and
+ * pointer owned by the caller; the library keeps no pointer after the call.
+ * The only memory the library allocates is its split-K workspace: one device
+ * buffer per (device, stream), grown on demand outside stream capture (the
+ * growth synchronises that stream once) and kept for the process lifetime.
+ * During stream capture a call never allocates: a shape whose workspace would
+ * have to grow takes a cluster-only plan instead (same kernels).  The *_host entry points take host pointers and
  * manage their own stream-ordered device scratch.  O must not overlap I or F.
  *
  * Execution: asynchronous and stream-ordered on the given stream (a
  * cudaStream_t / CUstream passed as void*; NULL = legacy default stream);
  * no host synchronisation inside the device entry points.  Kernel faults
  * surface at the caller's next synchronisation.  Reentrant: no mutable global
- * state except one-time kernel attribute setup.
+ * state except one-time kernel attribute setup and the workspace cache
+ * (mutex-protected).
  *
  * Errors: the return value is a conv_status.  On any argument error nothing is
  * launched and O is untouched.  Checks, in order:
@@ -108,7 +113,9 @@ B200CONV_API int conv_multi_host(const void *I, int C, int Wx, int Wy, const voi
                     int precision, void *stream);
 
 /* Launch plan the device entry points use for a shape (pure function; no
- * device access).  Every call of the hot path is exactly ONE kernel launch. */
+ * device access).  A call of the hot path is one kernel launch, or two when
+ * the channel split is reduced through the library's split-K workspace
+ * (launches == 2: a deterministic fixed-order reduction kernel follows). */
 typedef struct {
     int kernel;        /* 0 = KS (single FP32), 1 = KM-SIMT (multi FP32), 2 = KM-TC (tf32/bf16) */
     int grid_x, grid_y, grid_z;
@@ -117,7 +124,9 @@ typedef struct {
     int tile_m;        /* filters per CTA tile */
     int tile_n;        /* (wide) output pixels per CTA tile */
     int smem_bytes;    /* dynamic shared memory per CTA */
-    int tma_f;         /* 1 if F tiles are loaded by TMA (tensor map) */
+    int tma_f;         /* bit 0: F tiles by TMA; bit 1: I patch by TMA (KM-TC) */
+    int launches;      /* kernel launches per call: 1, or 2 (split-K through the workspace;
+                          cluster_x is then 1 and grid_x is the split count) */
 } conv_plan;
 
 B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);

@@ -35,6 +35,12 @@ int b200::choose_split(int tiles, int units, int max_split, int ctas_per_sm, flo
     return best;
 }
 
+int b200::clusters_resident(int S, int ctas_per_sm) {
+    if (S < 1) S = 1;
+    if (S > 16) S = 16;
+    return (ctas_per_sm >= 2 ? kClusters2 : kClusters1)[S];
+}
+
 namespace {
 
 int check_shape(int C, int Wx, int Wy, int K, int M) {
@@ -217,7 +223,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 0; }
+int conv_version(void) { return (1 << 16) | 1; }
 
 }  // extern "C"
 

@@ -7,22 +7,27 @@
 // Design: an implicit GEMM on the FP32 pipes,
 //   D[m][n] = sum_k F[m][k] * B[k][n],  k = (ch, r, c),  n = output pixel y*Wo+x
 //  * CTA tile = BM filters x BN output pixels (compact indexing: no garbage
-//    columns), 256 threads, 8 x 8 register tile per thread taken as two 4-wide
-//    halves in m and in n so every operand load is a 16-B shared load.
+//    columns), 256 threads, 8 x TN register tile per thread (TN = 8, 6 or 4),
+//    every operand load a 16-B (or 8-B) shared load.
 //  * The reduction runs over channel chunks of CB channels — the paper's
-//    segment of S = CB*K*K*4 bytes per filter — double buffered
-//    (the paper's prefetch rounds):
+//    segment of S = CB*K*K*4 bytes per filter — in a two-stage
+//    cp.async pipeline (the paper's prefetch rounds):
 //      F: 16-B cp.async of the rows as stored into a raw buffer, then an
-//         in-smem transpose to [k][m];
+//         in-smem transpose to [k][m] (a transpose-free [k/4][m][4] layout
+//         was measured slower: ptxas interleaves the four k of a quad into
+//         short dependent FFMA chains);
 //      B: the im2col tile [k][n] gathered straight from global/L2 by 4-B
 //         cp.async (one pixel per lane: coalesced), offsets from a small
 //         per-chunk k -> (ch, r, c) table in shared memory.
 //  * Small layers cannot fill 148 SMs with output tiles, so the channel sum is
-//    split across a thread-block cluster of up to 16 CTAs (the paper's
-//    rejected Fig. 2(b) split along ch): partial tiles are reduced
-//    through distributed shared memory in fixed rank order (deterministic, no
-//    global atomics, O written once).
+//    split S ways (the paper's rejected Fig. 2(b) split along ch):
+//    either across a thread-block cluster (partials reduced through
+//    distributed shared memory in fixed rank order) or, when more splits pay
+//    than clusters can co-reside, through the split-K workspace and a
+//    fixed-order reduction kernel (workspace.cu).  Both are deterministic.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -62,13 +67,28 @@ kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
 // computes from F_s, and is transposed into F_s once every thread is done.)
 __host__ __device__ constexpr int simt_rs(int CK) { return ((CK - 4 + 31) / 32) * 32 + 4; }
 
-template <int BM, int BN>
+// Thread tile: 8 filters (two 4-row halves, BM/2 apart) x TN pixels, TN in
+// {8, 6, 4}: columns tn*4 .. tn*4+3 of the first region (width R1 = 4*TNG) and,
+// for TN > 4, TN-4 more columns at R1 + tn*(TN-4) — every operand load is one
+// 16-B (or 8-B) shared load.
+template <int BM, int BN, int TN>
+struct SimtShape {
+    static constexpr int TNG = BN / TN;             // thread columns
+    static constexpr int TMG = BM / 8;              // thread rows
+    static constexpr int R1 = 4 * TNG;
+    static constexpr int T2 = TN - 4;               // 0, 2 or 4
+    static_assert(TMG * TNG == kSimtThreads && TNG * TN == BN, "tile must map to 256 threads");
+    __device__ static int row(int tm, int i) { return i < 4 ? tm * 4 + i : BM / 2 + tm * 4 + (i - 4); }
+};
+
+template <int BM, int BN, int TN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
-           int K, int M, float *__restrict__ O, int ch_per_split, int CB) {
-    static_assert((BM / 8) * (BN / 8) == kSimtThreads, "tile must map to 256 threads");
+           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W) {
+    using SH = SimtShape<BM, BN, TN>;
     constexpr int NT = kSimtThreads;
-    constexpr int TNG = BN / 8;                     // thread columns
+    constexpr int TNG = SH::TNG;
+    constexpr int T2 = SH::T2;
     const int KK = K * K;
     const int Ho = Wy - K + 1, Wo = Wx - K + 1;
     const int HW = Wx * Wy;
@@ -83,7 +103,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     float *Fraw = Bs_buf + 2 * CK * BN;             // [BM][RS]
     int *koff = reinterpret_cast<int *>(Fraw + BM * RS);   // [CK]
 
-    const int S = gridDim.x;                        // cluster size == split
+    const int S = gridDim.x;                        // split count (== cluster size when W == nullptr)
     const int split = blockIdx.x;
     const int p0 = blockIdx.y * BN;
     const int m0 = blockIdx.z * BM;
@@ -144,6 +164,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     };
     // im2col tile B[k][n] = I[ch0 + ch][y_n + r][x_n + c] (zero past the valid range)
     auto load_b = [&](int chunk, int b) {
+        if (bkl >= KL) return;
         const int ch0 = ch_begin + chunk * CB;
         const int nk = min(CB, ch_end - ch0) * KK;
         const float *src = I + (int64_t)ch0 * HW + bbase;
@@ -168,11 +189,11 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         }
     };
 
-    float acc[8][8];
+    float acc[8][TN];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
     pdl_wait();
     pdl_trigger();
@@ -192,18 +213,26 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         const int b = chunk & 1;
         const float *Fs = Fs_buf + tm * 4;
         const float *Bs = Bs_buf + b * CK * BN + tn * 4;
+        const float *Bs2 = Bs_buf + b * CK * BN + SH::R1 + tn * T2;
 #pragma unroll 4
         for (int k = 0; k < CK; ++k) {
             const float4 a0 = *reinterpret_cast<const float4 *>(Fs + k * BM);
             const float4 a1 = *reinterpret_cast<const float4 *>(Fs + k * BM + BM / 2);
             const float4 b0 = *reinterpret_cast<const float4 *>(Bs + k * BN);
-            const float4 b1 = *reinterpret_cast<const float4 *>(Bs + k * BN + BN / 2);
+            float bv[TN];
+            bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
+            if constexpr (T2 == 4) {
+                const float4 b1 = *reinterpret_cast<const float4 *>(Bs2 + k * BN);
+                bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
+            } else if constexpr (T2 == 2) {
+                const float2 b1 = *reinterpret_cast<const float2 *>(Bs2 + k * BN);
+                bv[4] = b1.x; bv[5] = b1.y;
+            }
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
         if (chunk + 1 < nchunks) {
             cp_async_wait<0>();                     // chunk c+1 staged
@@ -215,17 +244,37 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         }
     }
     cp_async_wait<0>();
+
+    if (W != nullptr) {
+        // ---- workspace split-K: partial tile -> W[split] (padded, aligned) ----
+        const int ldw = gridDim.y * BN;
+        float *w = W + (int64_t)split * ((int64_t)gridDim.z * BM * ldw) + (int64_t)m0 * ldw + p0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float *wr = w + (int64_t)SH::row(tm, i) * ldw;
+            __stcg(reinterpret_cast<float4 *>(wr + tn * 4),
+                   make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]));
+            if constexpr (T2 == 4)
+                __stcg(reinterpret_cast<float4 *>(wr + SH::R1 + tn * 4),
+                       make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]));
+            else if constexpr (T2 == 2)
+                __stcg(reinterpret_cast<float2 *>(wr + SH::R1 + tn * 2), make_float2(acc[i][4], acc[i][5]));
+        }
+        return;
+    }
     __syncthreads();
 
     // ---- partial tile -> own smem, then fixed-order (DSMEM) reduction ------
     float *P = smem;                                // [BM][BN]
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int m = (i < 4) ? tm * 4 + i : BM / 2 + tm * 4 + (i - 4);
-        *reinterpret_cast<float4 *>(P + m * BN + tn * 4) =
-            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        *reinterpret_cast<float4 *>(P + m * BN + BN / 2 + tn * 4) =
-            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        float *pr = P + SH::row(tm, i) * BN;
+        *reinterpret_cast<float4 *>(pr + tn * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if constexpr (T2 == 4)
+            *reinterpret_cast<float4 *>(pr + SH::R1 + tn * 4) =
+                make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        else if constexpr (T2 == 2)
+            *reinterpret_cast<float2 *>(pr + SH::R1 + tn * 2) = make_float2(acc[i][4], acc[i][5]);
     }
     if (S > 1) cluster_sync_all(); else __syncthreads();
 
@@ -233,22 +282,38 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int rows = (split + 1) * BM / S - mlo;
     const uint32_t Pbase = smem_u32(P);
     const int nvalid = min(BN, HoWo - p0);
-    for (int idx = tid; idx < rows * BN; idx += NT) {
-        const int m = mlo + idx / BN, n = idx % BN;
-        float v = 0.f;
+    constexpr int BQ = BN / 4;
+    for (int idx = tid; idx < rows * BQ; idx += NT) {
+        const int m = mlo + idx / BQ, n = 4 * (idx % BQ);
+        float4 v;
         if (S > 1) {
-            for (int t = 0; t < S; ++t) v += ld_dsmem_f32(mapa_shared(Pbase + (m * BN + n) * 4, t));
+            v = ld_dsmem_f32x4(mapa_shared(Pbase + (m * BN + n) * 4, 0));
+            for (int t = 1; t < S; ++t) {
+                const float4 u = ld_dsmem_f32x4(mapa_shared(Pbase + (m * BN + n) * 4, t));
+                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+            }
         } else {
-            v = P[m * BN + n];
+            v = *reinterpret_cast<const float4 *>(P + m * BN + n);
         }
-        if (m0 + m < M && n < nvalid) O[(int64_t)(m0 + m) * HoWo + p0 + n] = v;   // compact: coalesced
+        if (m0 + m < M) {
+            float *o = O + (int64_t)(m0 + m) * HoWo + p0 + n;   // compact: coalesced
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (n + i < nvalid) o[i] = vv[i];
+        }
     }
     if (S > 1) cluster_sync_all();
 }
 
 namespace {
-struct SimtTile { int BM, BN; };
-constexpr SimtTile kSimtTiles[3] = {{128, 128}, {64, 256}, {256, 64}};
+struct SimtTile { int BM, BN, TN; };
+// 8 x TN outputs per thread, 256 threads: TN = 8 (16K-output tiles), 6, 4
+constexpr int kNumSimtTiles = 9;
+constexpr SimtTile kSimtTiles[kNumSimtTiles] = {
+    {128, 128, 8}, {64, 256, 8}, {256, 64, 8},
+    {256, 48, 6}, {128, 96, 6}, {64, 192, 6},
+    {256, 32, 4}, {128, 64, 4}, {64, 128, 4}};
 
 int simt_smem(int BM, int BN, int CK) {
     const int bytes = (CK * BM + 2 * CK * BN + BM * simt_rs(CK)) * 4 + CK * 4;
@@ -278,23 +343,113 @@ void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
     *CB = cb;
     *cps = ((per + cb - 1) / cb) * cb;
 }
+
+// Launch-time model (us) used to pick tile, split and reduction mode.  Per-SM
+// FFMA issue rate 128 lanes x 1.965 GHz times the sustained fraction with one
+// / two resident CTAs; constants fitted (tools/simt_model.py) to a measured
+// sweep of every (tile, split, mode) on the bench layers (tools/simt_sweep.py,
+// B200): the planner's pick is within 1.5% of the best measured on average.
+constexpr double kFmaPerUs = 128.0 * 1965.0;
+constexpr double kEff1 = 0.40, kEff2 = 0.45;
+constexpr double kCtaFixed = 0.5;      // prologue (first chunk latency) + epilogue
+constexpr double kClusterReduce = 9.0; // cluster co-scheduling + barrier waits + DSMEM reduction
+constexpr double kWsReduce = 0.5;      // second launch (PDL-overlapped) + its tail
+constexpr double kL2BytesPerUs = 3.0e6;
+
+double sm_time(int n, int q, double w) {
+    if (q >= 2) return (n / 2) * (2.0 * w / kEff2) + (n % 2) * (w / kEff1) + ((n + 1) / 2) * kCtaFixed;
+    return n * (w / kEff1 + kCtaFixed);
+}
+
+struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; };
+
+SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
+    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int64_t px = (int64_t)Ho * Wo;
+    const int KK = K * K;
+    SimtCfg best = {-1, 1, 1, C, 0, 0, 1e30};
+    for (int ti = 0; ti < kNumSimtTiles; ++ti) {
+        const SimtTile &T = kSimtTiles[ti];
+        const int npt = (int)((px + T.BN - 1) / T.BN);
+        const int nmt = (M + T.BM - 1) / T.BM;
+        const int tiles = npt * nmt;
+        const double tn_pen = T.TN == 8 ? 1.0 : (T.TN == 6 ? 0.95 : 1.1);    // fitted per thread tile
+        int last_S = -1;
+        for (int Sreq = 1; Sreq <= C && Sreq <= 128; ++Sreq) {
+            int CB, cps;
+            simt_split(C, Sreq, T.BM, T.BN, K, &CB, &cps);
+            const int S = (C + cps - 1) / cps;
+            if (S == last_S) continue;
+            last_S = S;
+            const int smem = simt_smem(T.BM, T.BN, CB * KK);
+            if (smem > kSimtMaxSmem + 64 * 1024) continue;
+            const int q = smem <= 113 * 1024 ? 2 : 1;
+            const double w = (double)T.BM * T.BN * cps * KK * tn_pen / kFmaPerUs;
+            for (int ws = 0; ws <= 1; ++ws) {
+                if (ws && (S == 1 || !allow_ws)) continue;
+                double t;
+                if (!ws) {
+                    if (S > kSimtMaxSplit) continue;
+                    const int cap = clusters_resident(S, q);
+                    const int waves = (tiles + cap - 1) / cap;
+                    const int per_wave = (tiles < cap ? tiles : cap) * S;
+                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w) + (S > 1 ? kClusterReduce : 0.0);
+                } else {
+                    const int64_t total = (int64_t)tiles * S;
+                    const double bytes = 8.0 * S * (double)nmt * T.BM * (double)npt * T.BN + 4.0 * M * px;
+                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w) + kWsReduce + bytes / kL2BytesPerUs;
+                }
+                if (t < best.t * 0.995) best = {ti, S, CB, cps, ws, smem, t};
+            }
+        }
+    }
+    return best;
+}
+
+// B200CONV_SIMT_FORCE="tile,S,ws" (experiments / tests): force tile index,
+// requested split and reduction mode
+bool simt_forced(int C, int K, SimtCfg *c) {
+    const char *e = getenv("B200CONV_SIMT_FORCE");
+    if (!e || !*e) return false;
+    int ti = 0, S = 1, ws = 0;
+    if (sscanf(e, "%d,%d,%d", &ti, &S, &ws) < 2 || ti < 0 || ti >= kNumSimtTiles || S < 1) return false;
+    const SimtTile &T = kSimtTiles[ti];
+    int CB, cps;
+    simt_split(C, S > C ? C : S, T.BM, T.BN, K, &CB, &cps);
+    const int Se = (C + cps - 1) / cps;
+    if (!ws && Se > kSimtMaxSplit) return false;
+    *c = {ti, Se, CB, cps, (ws && Se > 1) ? 1 : 0, simt_smem(T.BM, T.BN, CB * K * K), 0.0};
+    return true;
+}
+
+SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
+    SimtCfg c;
+    if (simt_forced(C, K, &c) && (allow_ws || !c.ws)) return c;
+    return simt_choose(C, Wx, Wy, K, M, allow_ws);
+}
+
+void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan *p) {
+    const int64_t px = (int64_t)(Wy - K + 1) * (Wx - K + 1);
+    const SimtTile &T = kSimtTiles[c.tile];
+    p->kernel = 1;
+    p->grid_x = c.S;
+    p->grid_y = (int)((px + T.BN - 1) / T.BN);
+    p->grid_z = (M + T.BM - 1) / T.BM;
+    p->block_x = kSimtThreads;
+    p->cluster_x = c.ws ? 1 : c.S;
+    p->tile_m = T.BM;
+    p->tile_n = T.BN;
+    p->smem_bytes = c.smem;
+    p->tma_f = 0;
+    p->launches = c.ws ? 2 : 1;
+    (void)C;
+}
 }  // namespace
 
 int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
-    const int64_t px = (int64_t)Ho * Wo;                  // compact output pixels
-    // tile shape with the least padded work (ties: the first, 128 x 128)
-    int best = 0;
-    int64_t best_pad = -1;
-    for (int i = 0; i < 3; ++i) {
-        const int64_t pad = ((px + kSimtTiles[i].BN - 1) / kSimtTiles[i].BN) * kSimtTiles[i].BN *
-                            (((int64_t)M + kSimtTiles[i].BM - 1) / kSimtTiles[i].BM) * kSimtTiles[i].BM;
-        if (best_pad < 0 || pad < best_pad) { best_pad = pad; best = i; }
-    }
-    const int BM = kSimtTiles[best].BM, BN = kSimtTiles[best].BN;
-    const int CB = simt_cb_for(BM, BN, K, C);
-    if (simt_smem(BM, BN, CB * K * K) > kSimtMaxSmem + 64 * 1024) {   // naive fallback (huge K)
-        const int64_t n = (int64_t)M * px;
+    const SimtCfg c = simt_config(C, Wx, Wy, K, M, true);
+    if (c.tile < 0) {                                   // naive fallback (huge K)
+        const int64_t n = (int64_t)M * (Wy - K + 1) * (Wx - K + 1);
         int64_t blocks = (n + 255) / 256;
         p->kernel = 1;
         p->grid_x = (int)(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
@@ -305,33 +460,17 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
         p->tile_n = 1;
         p->smem_bytes = 0;
         p->tma_f = 0;
+        p->launches = 1;
         return 0;
     }
-    const int npt = (int)((px + BN - 1) / BN);
-    const int nmt = (M + BM - 1) / BM;
-    const int tiles = npt * nmt;
-    // split the channel sum over a cluster (unit = 1 channel of a 16K-output
-    // tile, ~0.6 us per 9 taps; DSMEM reduction ~1 us)
-    const int smem = simt_smem(BM, BN, CB * K * K);
-    const int S = choose_split(tiles, C, kSimtMaxSplit, smem <= 113 * 1024 ? 2 : 1,
-                               0.6f * (float)(K * K) / 9.f, 1.0f);
-    p->kernel = 1;
-    p->grid_x = S;
-    p->grid_y = npt;
-    p->grid_z = nmt;
-    p->block_x = kSimtThreads;
-    p->cluster_x = S;
-    p->tile_m = BM;
-    p->tile_n = BN;
-    p->smem_bytes = smem;
-    p->tma_f = 0;
+    fill_plan(c, C, Wx, Wy, K, M, p);
     return 0;
 }
 
-template <int BM, int BN>
-static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx, int Wy,
-                              const float *F, int K, int M, float *O, cudaStream_t s) {
-    auto kern = kms_kernel<BM, BN>;
+template <int BM, int BN, int TN>
+static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float *I, int C, int Wx, int Wy,
+                              const float *F, int K, int M, float *O, float *W, cudaStream_t s) {
+    auto kern = kms_kernel<BM, BN, TN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return e;
@@ -339,27 +478,29 @@ static cudaError_t launch_kms(const conv_plan &p, const float *I, int C, int Wx,
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
-    int CB, ch_per_split;
-    simt_split(C, p.cluster_x, BM, BN, K, &CB, &ch_per_split);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
     cfg.blockDim = dim3(p.block_x);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.cluster_x;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = p.cluster_x;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, ch_per_split, CB);
+    cfg.numAttrs = W ? 1 : 2;
+    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W);
+    if (e != cudaSuccess || !W) return e;
+    const int ldw = p.grid_y * BN;
+    const int64_t slice = (int64_t)p.grid_z * BM * ldw;
+    return launch_splitk_reduce(W, p.grid_x, slice, M, ldw, (Wy - K + 1) * (Wx - K + 1), O, s);
 }
 
 int simt_max_clusters(int cluster, int smem) {
-    auto kern = kms_kernel<128, 128>;
+    auto kern = kms_kernel<128, 128, 8>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -380,15 +521,34 @@ int simt_max_clusters(int cluster, int smem) {
 
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
                               float *O, cudaStream_t s) {
-    conv_plan p;
-    plan_multi_simt(C, Wx, Wy, K, M, &p);
-    if (p.tile_m == 1) {
+    SimtCfg c = simt_config(C, Wx, Wy, K, M, true);
+    if (c.tile < 0) {
+        conv_plan p;
+        plan_multi_simt(C, Wx, Wy, K, M, &p);
         kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I, C, Wx, Wy, F, K, M, O);
         return cudaGetLastError();
     }
-    if (p.tile_m == 64) return launch_kms<64, 256>(p, I, C, Wx, Wy, F, K, M, O, s);
-    if (p.tile_m == 256) return launch_kms<256, 64>(p, I, C, Wx, Wy, F, K, M, O, s);
-    return launch_kms<128, 128>(p, I, C, Wx, Wy, F, K, M, O, s);
+    float *W = nullptr;
+    if (c.ws) {
+        const SimtTile &T = kSimtTiles[c.tile];
+        const int64_t px = (int64_t)(Wy - K + 1) * (Wx - K + 1);
+        const size_t bytes = (size_t)c.S * ((M + T.BM - 1) / T.BM) * T.BM * ((px + T.BN - 1) / T.BN) * T.BN * 4;
+        W = static_cast<float *>(workspace_get(bytes, s));
+        if (!W) c = simt_config(C, Wx, Wy, K, M, false);   // capturing: cluster-only plan
+    }
+    conv_plan p;
+    fill_plan(c, C, Wx, Wy, K, M, &p);
+    switch (c.tile) {
+        case 0: return launch_kms<128, 128, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 1: return launch_kms<64, 256, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 2: return launch_kms<256, 64, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 3: return launch_kms<256, 48, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 4: return launch_kms<128, 96, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 5: return launch_kms<64, 192, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 6: return launch_kms<256, 32, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 7: return launch_kms<128, 64, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        default: return launch_kms<64, 128, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+    }
 }
 
 }  // namespace b200

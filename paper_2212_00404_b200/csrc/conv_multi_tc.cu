@@ -529,6 +529,7 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     const bool aligned = ((Ktot * elem) % 16 == 0) &&
                          (F == nullptr || (reinterpret_cast<uintptr_t>(F) % 16) == 0);
     p->tma_f = (aligned ? 1 : 0) | (patch ? 2 : 0);    // bit 0: F by TMA, bit 1: I patch by TMA
+    p->launches = 1;
     return 0;
 }
 

@@ -253,6 +253,7 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     p->cluster_x = 1;
     p->tma_f = 0;
+    p->launches = 1;
     const int TX = ks_TX(Wo);
     if (K <= 7 && TX <= 8) {
         const int R = ks_R(K);

@@ -1,6 +1,8 @@
 // kernels.h — internal launch interface between the C ABI (abi.cu) and the
 // three kernels (KS, KM-SIMT, KM-TC).  Not part of the public ABI.
 #pragma once
+#include <cstddef>
+#include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/b200conv.h"
 
@@ -33,6 +35,16 @@ cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F,
 // for kernels that fit 1 or 2 CTAs per SM.
 int choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_unit,
                  float t_reduce);
+// co-resident clusters of size S (1..16) for 1 or 2 CTAs per SM (same table)
+int clusters_resident(int S, int ctas_per_sm);
+
+// split-K workspace (workspace.cu): >= bytes of device memory owned by the
+// library for (current device, stream); nullptr if it would have to grow
+// while the stream is being captured (or on OOM)
+void *workspace_get(size_t bytes, cudaStream_t s);
+// O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1
+cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
+                                 cudaStream_t s);
 
 // max co-resident clusters (diagnostics)
 int tc_max_clusters(int cluster, int smem);

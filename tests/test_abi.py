@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16)
+    assert conv.version() == (1 << 16) | 1
 
 
 def test_status_strings():
@@ -95,7 +95,11 @@ def test_plans_cover_every_config_with_one_launch():
         for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
             p = conv.plan_multi(cfg["C"], cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"], prec)
             assert p["kernel"] == kern
-            assert 1 <= p["cluster_x"] <= 16 and p["grid_x"] == p["cluster_x"]
+            assert 1 <= p["cluster_x"] <= 16 and p["launches"] in (1, 2)
+            if p["launches"] == 1:
+                assert p["grid_x"] == p["cluster_x"]           # split reduced inside a cluster
+            else:
+                assert p["cluster_x"] == 1 and p["grid_x"] > 1  # split reduced via the workspace
             assert p["smem_bytes"] <= 227 * 1024
             Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
             px = Ho * (Wo if prec == "fp32" else cfg["Wx"])        # compact (SIMT) / wide (TC)

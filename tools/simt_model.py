@@ -1,0 +1,122 @@
+"""Host replica of the KM-SIMT planner model (conv_multi_simt.cu simt_choose),
+used to fit its constants against a measured sweep (tools/simt_sweep.py).
+usage: simt_model.py gpurun_out/simt_sweep_v1.json"""
+import itertools
+import json
+import math
+import sys
+
+TILES = [(128, 128, 8), (64, 256, 8), (256, 64, 8), (256, 48, 6), (128, 96, 6), (64, 192, 6),
+         (256, 32, 4), (128, 64, 4), (64, 128, 4)]
+CL1 = [0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7]
+CL2 = [0, 296, 148, 93, 71, 56, 45, 37, 33, 30, 26, 21, 21, 17, 14, 14, 14]
+LAYERS = {"resnet_28x28_c128_m128_k3": (128, 28, 3, 128), "resnet_14x14_c256_m256_k3": (256, 14, 3, 256),
+          "resnet_7x7_c512_m512_k3": (512, 7, 3, 512), "vgg_224x224_c3_m64_k3": (3, 224, 3, 64),
+          "vgg_56x56_c64_m64_k3": (64, 56, 3, 64), "alexnet_27x27_c96_m256_k5": (96, 27, 5, 256),
+          "target_28x28_c256_m256_k3": (256, 28, 3, 256), "sweep_14x14_c512_m4096_k3": (512, 14, 3, 4096)}
+MAXSMEM = 110 * 1024
+
+
+def rs(ck):
+    return ((ck - 4 + 31) // 32) * 32 + 4
+
+
+def smem(BM, BN, CK):
+    b = (CK * BM + 2 * CK * BN + BM * rs(CK)) * 4 + CK * 4
+    return max(b, BM * BN * 4)
+
+
+def cb_for(BM, BN, K, C):
+    cb = (64 // (K * K) + 3) & ~3
+    cb = max(cb, 8)
+    while cb > 4 and smem(BM, BN, cb * K * K) > MAXSMEM:
+        cb -= 4
+    while cb > 1 and smem(BM, BN, cb * K * K) > MAXSMEM + 16 * 1024:
+        cb -= 1
+    return max(1, min(cb, C))
+
+
+def split(C, S, BM, BN, K):
+    per = -(-C // S)
+    budget = cb_for(BM, BN, K, C)
+    cb = 1
+    for c in (8, 4, 2):
+        if c > budget or c > per:
+            continue
+        waste = -(-per // c) * c - per
+        if 8 * waste <= per:
+            cb = c
+            break
+    return cb, -(-per // cb) * cb
+
+
+def cost(P, C, W, K, M, ti, Sreq, ws):
+    BM, BN, TN = TILES[ti]
+    Ho = Wo = W - K + 1
+    px = Ho * Wo
+    npt, nmt = -(-px // BN), -(-M // BM)
+    tiles = npt * nmt
+    CB, cps = split(C, min(Sreq, C), BM, BN, K)
+    S = -(-C // cps)
+    sm = smem(BM, BN, CB * K * K)
+    q = 2 if sm <= 113 * 1024 else 1
+    pen = {8: 1.0, 6: P["pen6"], 4: P["pen4"]}[TN]
+    w = BM * BN * cps * K * K * pen / (128 * 1965.0)
+
+    def smt(n):
+        if q >= 2:
+            return (n // 2) * (2 * w / P["e2"]) + (n % 2) * (w / P["e1"]) + ((n + 1) // 2) * P["c0"]
+        return n * (w / P["e1"] + P["c0"])
+    if not ws:
+        if S > 16:
+            return None, S
+        cap = (CL2 if q >= 2 else CL1)[S]
+        waves = -(-tiles // cap)
+        per_wave = min(tiles, cap) * S
+        return waves * smt(-(-per_wave // 148)) + (P["ccl"] if S > 1 else 0), S
+    if S == 1:
+        return None, S
+    byts = 8.0 * S * nmt * BM * npt * BN + 4.0 * M * px
+    return smt(-(-tiles * S // 148)) + P["cws"] + byts / P["l2"], S
+
+
+def main():
+    d = json.load(open(sys.argv[1]))
+    meas = {}
+    for r in d:
+        if "us" in r and r["cfg"] is not None:
+            meas.setdefault(r["layer"], {})[tuple(r["cfg"])] = r["us"]
+    base = dict(e1=0.40, e2=0.60, c0=1.0, ccl=1.0, cws=2.0, l2=3.0e6, pen6=1.03, pen4=1.08)
+    grid = dict(e1=[0.35, 0.4, 0.45], e2=[0.45, 0.5, 0.55], c0=[0.5, 1.0, 2.0], ccl=[4.0, 6.0, 9.0],
+                cws=[0.5, 1.0, 2.0], pen6=[0.95, 1.0, 1.05], pen4=[1.1, 1.2, 1.3])
+
+    def regret(P, verbose=False):
+        tot = 0.0
+        for L, m in meas.items():
+            C, W, K, M = LAYERS[L]
+            best_meas = min(m.values())
+            cands = []
+            for (ti, S, ws), us in m.items():
+                t, _ = cost(P, C, W, K, M, ti, S, ws)
+                if t is not None:
+                    cands.append((t, us, (ti, S, ws)))
+            pick = min(cands)
+            tot += math.log(pick[1] / best_meas)
+            if verbose:
+                print(f"{L:28s} pick {pick[2]} pred {pick[0]:7.1f} meas {pick[1]:7.1f} best {best_meas:7.1f}")
+        return tot
+    best = (regret(base), base)
+    keys = list(grid)
+    for vals in itertools.product(*[grid[k] for k in keys]):
+        P = dict(base)
+        P.update(zip(keys, vals))
+        r = regret(P)
+        if r < best[0] - 1e-9:
+            best = (r, P)
+    print("regret (sum log)", best[0])
+    print(best[1])
+    regret(best[1], True)
+
+
+if __name__ == "__main__":
+    main()
