@@ -352,13 +352,15 @@ void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
 constexpr double kFmaPerUs = 128.0 * 1965.0;
 constexpr double kEff1 = 0.40, kEff2 = 0.45;
 constexpr double kCtaFixed = 0.5;      // prologue (first chunk latency) + epilogue
+constexpr double kPerChunk = 0.6;      // per channel chunk: barriers, F transpose, load issue
 constexpr double kClusterReduce = 9.0; // cluster co-scheduling + barrier waits + DSMEM reduction
 constexpr double kWsReduce = 0.5;      // second launch (PDL-overlapped) + its tail
 constexpr double kL2BytesPerUs = 3.0e6;
 
-double sm_time(int n, int q, double w) {
-    if (q >= 2) return (n / 2) * (2.0 * w / kEff2) + (n % 2) * (w / kEff1) + ((n + 1) / 2) * kCtaFixed;
-    return n * (w / kEff1 + kCtaFixed);
+double sm_time(int n, int q, double w, int nch) {
+    const double c = kCtaFixed + nch * kPerChunk;
+    if (q >= 2) return (n / 2) * (2.0 * w / kEff2) + (n % 2) * (w / kEff1) + ((n + 1) / 2) * c;
+    return n * (w / kEff1 + c);
 }
 
 struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; };
@@ -373,9 +375,9 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
         const int npt = (int)((px + T.BN - 1) / T.BN);
         const int nmt = (M + T.BM - 1) / T.BM;
         const int tiles = npt * nmt;
-        const double tn_pen = T.TN == 8 ? 1.0 : (T.TN == 6 ? 0.95 : 1.1);    // fitted per thread tile
+        const double tn_pen = T.TN == 8 ? 1.0 : (T.TN == 6 ? 0.9 : 1.0);     // fitted per thread tile
         int last_S = -1;
-        for (int Sreq = 1; Sreq <= C && Sreq <= 128; ++Sreq) {
+        for (int Sreq = 1; Sreq <= C && Sreq <= 96; ++Sreq) {
             int CB, cps;
             simt_split(C, Sreq, T.BM, T.BN, K, &CB, &cps);
             const int S = (C + cps - 1) / cps;
@@ -385,6 +387,7 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
             if (smem > kSimtMaxSmem + 64 * 1024) continue;
             const int q = smem <= 113 * 1024 ? 2 : 1;
             const double w = (double)T.BM * T.BN * cps * KK * tn_pen / kFmaPerUs;
+            const int nch = (cps + CB - 1) / CB;
             for (int ws = 0; ws <= 1; ++ws) {
                 if (ws && (S == 1 || !allow_ws)) continue;
                 double t;
@@ -393,11 +396,11 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
                     const int cap = clusters_resident(S, q);
                     const int waves = (tiles + cap - 1) / cap;
                     const int per_wave = (tiles < cap ? tiles : cap) * S;
-                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w) + (S > 1 ? kClusterReduce : 0.0);
+                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w, nch) + (S > 1 ? kClusterReduce : 0.0);
                 } else {
                     const int64_t total = (int64_t)tiles * S;
                     const double bytes = 8.0 * S * (double)nmt * T.BM * (double)npt * T.BN + 4.0 * M * px;
-                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w) + kWsReduce + bytes / kL2BytesPerUs;
+                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w, nch) + kWsReduce + bytes / kL2BytesPerUs;
                 }
                 if (t < best.t * 0.995) best = {ti, S, CB, cps, ws, smem, t};
             }

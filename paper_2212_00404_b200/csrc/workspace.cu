@@ -7,14 +7,15 @@
 // memory inside one thread-block cluster; beyond that (or when clusters of the
 // needed size do not co-reside) each split writes its partial tile to a
 // device workspace W[S][Mpad][Npad] and `splitk_reduce_kernel` sums the S
-// slices in fixed order s = 0..S-1 (deterministic: no atomics) into the
-// compact O[M][Ho*Wo].
+// slices in a fixed order (deterministic: no atomics) into the compact
+// O[M][Ho*Wo].
 //
 // The workspace is owned by the library: one buffer per (device, stream),
 // grown (never shrunk) on demand outside stream capture; a call made while
 // the stream is being captured that would need a bigger buffer gets nullptr
 // and the caller falls back to a cluster-only plan.
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -53,36 +54,67 @@ void *workspace_get(size_t bytes, cudaStream_t s) {
 
 // O[m][n] = sum_{s=0}^{S-1} W[s][m][n], m < M, n < N (compact O, row stride N;
 // W rows padded to ldw, a multiple of 4; slice = Mpad * ldw floats).
+// G (1 or 8) adjacent lanes share one float4 of outputs: lane g sums the
+// slices s = g, g + G, ... in order (8 loads in flight), then the G lane sums
+// combine by a fixed xor tree — the same order on every run, so the result is
+// deterministic.
+template <int kRedG>
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, int ldw, int N,
                      float *__restrict__ O) {
     pdl_wait();
     pdl_trigger();
+    // 32-bit indexing: M * N <= INT_MAX is an ABI precondition
     const int q_per_row = (N + 3) >> 2;
-    const int64_t total = (int64_t)M * q_per_row;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const int m = (int)(u / q_per_row);
-        const int n = 4 * (int)(u - (int64_t)m * q_per_row);
+    const int total = M * q_per_row;
+    const int g = threadIdx.x % kRedG;
+    constexpr int kGroupsPerWarp = 32 / kRedG;
+    const int stride = gridDim.x * (blockDim.x / kRedG);
+    // warp-uniform trip count (the shuffles below need all 32 lanes)
+    for (int ub = blockIdx.x * (blockDim.x / kRedG) + (threadIdx.x / 32) * kGroupsPerWarp; ub < total;
+         ub += stride) {
+        const int u = ub + (threadIdx.x % 32) / kRedG;
+        const bool valid = u < total;
+        const int m = valid ? u / q_per_row : 0;
+        const int n = valid ? 4 * (u - m * q_per_row) : 0;
         const float *w = W + (int64_t)m * ldw + n;
-        float4 a = __ldcs(reinterpret_cast<const float4 *>(w));
-        for (int s = 1; s < S; ++s) {
-            const float4 b = __ldcs(reinterpret_cast<const float4 *>(w + s * slice));
-            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-        }
-        float *o = O + (int64_t)m * N + n;
-        const float v[4] = {a.x, a.y, a.z, a.w};
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int Sv = valid ? S : 0;
+        // 8 loads in flight per lane (the partials sit in L2: latency-bound)
+        for (int s0 = g; s0 < Sv; s0 += 8 * kRedG) {
+            float4 b[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (n + i < N) o[i] = v[i];
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j * kRedG < Sv) b[j] = __ldcs(reinterpret_cast<const float4 *>(w + (s0 + j * kRedG) * slice));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j * kRedG < Sv) { a.x += b[j].x; a.y += b[j].y; a.z += b[j].z; a.w += b[j].w; }
+        }
+#pragma unroll
+        for (int o = kRedG / 2; o >= 1; o >>= 1) {   // (no-op for kRedG == 1)
+            a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+            a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+            a.z += __shfl_xor_sync(0xffffffffu, a.z, o);
+            a.w += __shfl_xor_sync(0xffffffffu, a.w, o);
+        }
+        if (valid && g == 0) {
+            float *o = O + (int64_t)m * N + n;
+            const float v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (n + i < N) o[i] = v[i];
+        }
     }
 }
 
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
                                  cudaStream_t s) {
+    // few splits: one lane per float4 of outputs; many: 8 lanes (latency)
+    const char *e = getenv("B200CONV_REDG");
+    const int G = e ? atoi(e) : (S > 16 ? 8 : 1);
     const int64_t total = (int64_t)M * ((N + 3) / 4);
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    int64_t blocks = (total * G + 255) / 256;          // one float4 group per G lanes
+    if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;        // grid-stride: CTA launch rate, not work, bounds tiny CTAs
     if (blocks < 1) blocks = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
@@ -93,7 +125,8 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, W, S, slice, M, ldw, N, O);
+    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8>, W, S, slice, M, ldw, N, O);
+    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1>, W, S, slice, M, ldw, N, O);
 }
 
 }  // namespace b200

@@ -62,11 +62,13 @@ def cost(P, C, W, K, M, ti, Sreq, ws):
     q = 2 if sm <= 113 * 1024 else 1
     pen = {8: 1.0, 6: P["pen6"], 4: P["pen4"]}[TN]
     w = BM * BN * cps * K * K * pen / (128 * 1965.0)
+    nch = -(-cps // CB)
 
     def smt(n):
+        c = P["c0"] + nch * P["cch"]
         if q >= 2:
-            return (n // 2) * (2 * w / P["e2"]) + (n % 2) * (w / P["e1"]) + ((n + 1) // 2) * P["c0"]
-        return n * (w / P["e1"] + P["c0"])
+            return (n // 2) * (2 * w / P["e2"]) + (n % 2) * (w / P["e1"]) + ((n + 1) // 2) * c
+        return n * (w / P["e1"] + c)
     if not ws:
         if S > 16:
             return None, S
@@ -77,7 +79,29 @@ def cost(P, C, W, K, M, ti, Sreq, ws):
     if S == 1:
         return None, S
     byts = 8.0 * S * nmt * BM * npt * BN + 4.0 * M * px
-    return smt(-(-tiles * S // 148)) + P["cws"] + byts / P["l2"], S
+    lat = P["rsl"] * (S / 8.0 if S > 16 else S)          # serial partial loads per reduce lane
+    return smt(-(-tiles * S // 148)) + P["cws"] + byts / P["l2"] + lat, S
+
+
+def choose(P, C, W, K, M):
+    """Exactly the C++ search: tiles in order, Sreq 1..96 deduped by effective S,
+    cluster then workspace, keep the first within 0.5%."""
+    best = None
+    for ti, (BM, BN, TN) in enumerate(TILES):
+        last = -1
+        for Sreq in range(1, min(C, 96) + 1):
+            _, cps = split(C, Sreq, BM, BN, K)
+            S = -(-C // cps)
+            if S == last:
+                continue
+            last = S
+            for ws in (0, 1):
+                t, _ = cost(P, C, W, K, M, ti, Sreq, ws)
+                if t is None:
+                    continue
+                if best is None or t < best[0] * 0.995:
+                    best = (t, (ti, S, ws))
+    return best
 
 
 def main():
@@ -85,25 +109,25 @@ def main():
     meas = {}
     for r in d:
         if "us" in r and r["cfg"] is not None:
-            meas.setdefault(r["layer"], {})[tuple(r["cfg"])] = r["us"]
-    base = dict(e1=0.40, e2=0.60, c0=1.0, ccl=1.0, cws=2.0, l2=3.0e6, pen6=1.03, pen4=1.08)
-    grid = dict(e1=[0.35, 0.4, 0.45], e2=[0.45, 0.5, 0.55], c0=[0.5, 1.0, 2.0], ccl=[4.0, 6.0, 9.0],
-                cws=[0.5, 1.0, 2.0], pen6=[0.95, 1.0, 1.05], pen4=[1.1, 1.2, 1.3])
+            ti, Sreq, ws = r["cfg"]
+            C, W, K, M = LAYERS[r["layer"]]
+            BM, BN, TN = TILES[ti]
+            _, cps = split(C, min(Sreq, C), BM, BN, K)
+            meas.setdefault(r["layer"], {})[(ti, -(-C // cps), ws)] = r["us"]
+    base = dict(e1=0.40, e2=0.45, c0=0.5, ccl=9.0, cws=0.5, l2=3.0e6, pen6=0.95, pen4=1.1, rsl=0.0, cch=0.0)
+    grid = dict(e2=[0.45, 0.5], cws=[0.5, 1.0], pen6=[0.9, 0.95, 1.0], pen4=[1.0, 1.1, 1.2],
+                rsl=[0.0, 0.05], cch=[0.3, 0.4, 0.6, 0.8], e1=[0.35, 0.4, 0.45])
 
     def regret(P, verbose=False):
         tot = 0.0
         for L, m in meas.items():
             C, W, K, M = LAYERS[L]
             best_meas = min(m.values())
-            cands = []
-            for (ti, S, ws), us in m.items():
-                t, _ = cost(P, C, W, K, M, ti, S, ws)
-                if t is not None:
-                    cands.append((t, us, (ti, S, ws)))
-            pick = min(cands)
-            tot += math.log(pick[1] / best_meas)
+            t, cfg = choose(P, C, W, K, M)
+            us = m.get(cfg, best_meas * 2)
+            tot += math.log(us / best_meas)
             if verbose:
-                print(f"{L:28s} pick {pick[2]} pred {pick[0]:7.1f} meas {pick[1]:7.1f} best {best_meas:7.1f}")
+                print(f"{L:28s} pick {cfg} pred {t:7.1f} meas {us:7.1f} best {best_meas:7.1f}")
         return tot
     best = (regret(base), base)
     keys = list(grid)

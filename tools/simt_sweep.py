@@ -9,6 +9,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import torch
 import torch.nn.functional as Fn
 
@@ -61,8 +62,23 @@ for L in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
     scale = float(ref.abs().max())
     cfgs = [None]
     C = L["C"]
-    Ss = sorted({s for s in (1, 2, 3, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 40, 48, 64, 96) if s <= C})
-    for ti in range(len(TILES)):
+    if "--dense" in sys.argv:
+        import simt_model
+        for ti, (BM, BN, TN) in enumerate(simt_model.TILES):
+            seen = set()
+            for S in range(1, min(C, 96) + 1):
+                cb, cps = simt_model.split(C, S, BM, BN, L["K"])
+                Se = -(-C // cps)
+                if Se in seen:
+                    continue
+                seen.add(Se)
+                for ws in (0, 1):
+                    if (ws == 0 and Se > 16) or (ws == 1 and Se == 1):
+                        continue
+                    cfgs.append((ti, S, ws))
+    Ss = [] if "--dense" in sys.argv else sorted(
+        {s for s in (1, 2, 3, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 40, 48, 64, 96) if s <= C})
+    for ti in range(len(TILES) if Ss else 0):
         for S in Ss:
             for ws in (0, 1):
                 if (ws == 0 and S > 16) or (ws == 1 and S == 1):
