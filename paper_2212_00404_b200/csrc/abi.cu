@@ -5,6 +5,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 #include "kernels.h"
 
@@ -126,12 +127,40 @@ int conv_multi(const float *I, int C, int Wx, int Wy, const float *F, int K, int
 }
 
 // ------------------------------------------------------------ host buffers
+// Library-owned stream-ordered pool per device with no release threshold: the
+// device staging buffers of the host entry points are recycled across calls
+// instead of being returned to the driver at every synchronisation.
+static cudaMemPool_t host_pool() {
+    static cudaMemPool_t pools[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = p;
+    }
+    return pools[dev];
+}
+
+static cudaError_t pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t p = host_pool();
+    return p ? cudaMallocFromPoolAsync(ptr, bytes, p, s) : cudaMallocAsync(ptr, bytes, s);
+}
+
 static int host_roundtrip(const void *Ih, size_t i_bytes, const void *Fh, size_t f_bytes, float *Oh,
                           size_t o_bytes, cudaStream_t s,
                           int (*body)(const void *, const void *, float *, void *), void *ctx) {
     void *Id = nullptr, *Fd = nullptr, *Od = nullptr;
-    if (cudaMallocAsync(&Id, i_bytes, s) != cudaSuccess || cudaMallocAsync(&Fd, f_bytes, s) != cudaSuccess ||
-        cudaMallocAsync(&Od, o_bytes, s) != cudaSuccess) {
+    if (pool_alloc(&Id, i_bytes, s) != cudaSuccess || pool_alloc(&Fd, f_bytes, s) != cudaSuccess ||
+        pool_alloc(&Od, o_bytes, s) != cudaSuccess) {
         cudaGetLastError();
         if (Id) cudaFreeAsync(Id, s);
         if (Fd) cudaFreeAsync(Fd, s);
@@ -230,6 +259,7 @@ int conv_version(void) { return (1 << 16) | 1; }
 // ------------------------------------------------------------ diagnostics
 // Max co-resident clusters for a kernel family at a cluster size (tools only).
 extern "C" B200CONV_API int conv_diag_stamps(unsigned long long *host) { return tc_read_stamps(host); }
+extern "C" B200CONV_API int conv_diag_ks_stamps(unsigned long long *host) { return ks_read_stamps(host); }
 extern "C" B200CONV_API int conv_diag_max_clusters(int kernel, int cluster, int smem_bytes) {
     return kernel == 2 ? tc_max_clusters(cluster, smem_bytes) : simt_max_clusters(cluster, smem_bytes);
 }

@@ -6,22 +6,26 @@
 //
 // For K <= 3 the output stream (O is >= 94 % of all bytes for Wx >= 56) binds
 // to HBM; for K >= 5 the FP32 FMA pipe binds.  Design:
-//  * One CTA owns a band of TY full output rows and a chunk of filters.  Because
-//    the band spans whole rows, O[m][y0 : y0+TY][:] is ONE contiguous range of
-//    TY*Wo floats per filter.  The paper's "only the feature maps are divided
-//    ... processed by all filters" option at CTA level: the halo
-//    band I[y0 .. y0+TY+K-1) is staged once in shared memory and reused for
-//    every filter of the chunk ("FMA operations per loaded data").
-//  * Filters are processed in groups of R; their taps sit in registers
-//    ("filters fully to registers").  Each thread computes R filters
-//    x 4 consecutive pixels (16-B shared loads of the input window, sliding
-//    window reuse across the K taps of a row).
-//  * Results go to a double-buffered shared-memory image of the contiguous
-//    output range (laid out so that smem and global addresses agree mod 16 B)
-//    and leave through ONE bulk TMA store per filter (cp.async.bulk
-//    shared->global): the write stream costs no per-element instructions.
-//    The <= 3 unaligned head/tail elements of a range are stored by threads.
+//  * Work is a grid of tasks (a block of RB full-width output rows) x (a group
+//    of R filters), each cut into 32-lane segments; the segments of the whole
+//    problem are dealt to ALL warps of one wave (3 CTAs x 8 warps per SM) in
+//    contiguous ranges that differ by at most one segment, so every SM gets the
+//    same work (no ragged last wave, no idle SMs) — the B200 counterpart of the
+//    paper's SM-assignment scheme (§3.1, Eqs. 4-9).
+//  * A CTA's range covers a contiguous band of row blocks: the band's input
+//    rows (ONE contiguous range of I) and the taps of its filter groups are
+//    staged once in shared memory with cp.async — "only the feature maps are
+//    divided ... processed by all filters", maximising FMAs per
+//    loaded byte.  Taps of the current group sit in registers
+//    ("filters fully to registers").
+//  * A lane computes TX consecutive pixels x RR consecutive rows x R filters
+//    from a (RR+K-1) x (TX+K-1) shared-memory window (vector loads; an input
+//    row feeds min(RR, K) output rows), and writes each (row, filter) result
+//    as VS-wide vector stores.  Consecutive lanes own consecutive pixels of a
+//    row, so every warp store is coalesced.  VS divides Wo, so stores stay
+//    aligned for any output offset.
 #include <cstdint>
+#include <cstdlib>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -29,109 +33,177 @@ namespace b200 {
 
 constexpr int kKsThreads = 256;
 constexpr int kKsWarps = kKsThreads / 32;
+// resident CTAs per SM: 3 (24 warps, <= 80 registers) for the store-bound small
+// K; 2 (16 warps, <= 128 registers) for the FMA-bound K >= 5, whose 4 x 4 pixel
+// register tiles need the room
+__host__ __device__ constexpr int ks_min_blocks(int K) { return K >= 5 ? 2 : 3; }
 
-// One work item = (row block, filter group): a warp computes RI output rows
-// x R filters.  Normal mode (rows >= 16 px): lane l owns TX consecutive pixels of
-// RR rows (vertical register blocking: an input row feeds up to min(RR, K)
-// output rows).  Small-map mode (TX == 1, Wo <= 16): the warp's lanes cover
-// RW = 32 / Wo whole rows, one pixel each.  Warps run independently after the
-// staging barrier: each writes its tile into a warp-private double-buffered
-// smem image of the contiguous global range O[m][y : y+RI][:], and lanes
-// 0..R-1 each stream one filter's range out with a bulk store.
-template <int K, int R, int TX, int RR>
-__global__ void __launch_bounds__(kKsThreads)
-ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__ F, int M,
-          float *__restrict__ O, int m_per_cta, int TY) {
+// Launch parameters of one KS call (computed by plan_ks on the host).
+struct KsArgs {
+    const float *I;
+    const float *F;
+    float *O;
+    int Wx, Wy, M;
+    int L;        // lane slots per output row: ceil(Wo / TX)
+    int RWt;      // row groups (of RR rows) per task: a task is RB = RWt*RR rows x R filters
+    int NG;       // filter groups ceil(M / R)
+    int nseg;     // 32-slot segments per task: ceil(RWt * L / 32)
+    int U;        // work units = tasks * nseg   (task t = (row block t / NG, group t % NG))
+    int NW;       // warps in the grid
+    int ub, ur;   // U = ub * NW + ur: warp w owns units [w*ub + min(w, ur), (w+1)*ub + min(w+1, ur))
+    int gmax;     // filter-group capacity of the smem tap table
+    int dbg;      // diagnostics: 1 = per-CTA globaltimer stamps into g_ks_stamps
+};
+
+// diagnostics (B200CONV_KS_DBG=1): per CTA [start, after griddepcontrol.wait,
+// staged, done << 8 | smid] globaltimer stamps of the last launch, CTAs 0..1023
+__device__ unsigned long long g_ks_stamps[4 * 1024];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+int ks_read_stamps(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_ks_stamps, sizeof(g_ks_stamps)) == cudaSuccess ? 0 : 1;
+}
+
+template <int V>
+__device__ __forceinline__ void lds_vec(const float *p, float *d) {
+    if constexpr (V == 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(p);
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    } else if constexpr (V == 2) {
+        const float2 v = *reinterpret_cast<const float2 *>(p);
+        d[0] = v.x; d[1] = v.y;
+    } else {
+        d[0] = *p;
+    }
+}
+template <int V>
+__device__ __forceinline__ void stg_vec(float *p, const float *v) {
+    if constexpr (V == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else if constexpr (V == 2) *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+    else *p = v[0];
+}
+
+// Work unit = one 32-slot segment of one task.  Slot s of a task = (row group
+// rg = s / L, column slot xv = s % L); its lane computes pixels x = TX*xv ..
+// x+TX-1 (the last slot of a row may be partial) of rows y0 .. y0+RR-1.
+// Loads are VL-wide (VL | Wx and the I alignment), stores VS-wide (VS | Wo).
+template <int K, int TX, int VL, int VS, int R, int RR>
+__global__ void __launch_bounds__(kKsThreads, ks_min_blocks(K))
+ks_kernel(const KsArgs a) {
     constexpr int KK = K * K;
     constexpr int GS = (R * KK + 3) & ~3;            // floats per filter group (16-B rows)
-    constexpr int WN = TX + K - 1;                   // input window per lane and row
+    constexpr int NV = (TX + K - 1 + VL - 1) / VL;   // load vectors per window row
     extern __shared__ __align__(16) float smem[];
+    const int Wx = a.Wx, Wy = a.Wy, M = a.M, L = a.L, NG = a.NG, nseg = a.nseg;
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
-    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;      // small-map rows per warp
-    const int RI = RW > 1 ? RW : RR;                          // output rows per item
-    const int SW = ((RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
-    const int y0 = blockIdx.y * TY;
-    const int rows = min(TY, Ho - y0);
-    const int n_ri = (rows + RI - 1) / RI;
-    const int CHW = ((RI * Wo + 3) & ~3) + 4;        // smem floats per (filter) output image
-    const int mc0 = blockIdx.x * m_per_cta;
-    const int mc1 = min(M, mc0 + m_per_cta);
-    const int ngroups = (mc1 - mc0 + R - 1) / R;
+    const int RB = a.RWt * RR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t plane = (int64_t)Ho * Wo;
+    const bool stamp = a.dbg && tid == 0 && blockIdx.x < 1024;
+    if (stamp) g_ks_stamps[4 * blockIdx.x] = gtimer();
 
-    float *s_w = smem;                                           // [groups][GS]
-    float *s_in = s_w + ((m_per_cta + R - 1) / R) * GS;          // (TY+K-1) x SW
-    float *s_out = s_in + (TY + K - 1) * SW + warp * 2 * R * CHW; // this warp: [2][R][CHW]
+    // this CTA's unit range -> task range -> row blocks and filter groups
+    // (all decoding happens before griddepcontrol.wait: it overlaps the
+    // previous kernel's tail)
+    const int c0 = blockIdx.x * kKsWarps;
+    const int u0 = c0 * a.ub + min(c0, a.ur);
+    const int u1 = (c0 + kKsWarps) * a.ub + min(c0 + kKsWarps, a.ur);
+    if (u0 >= u1) { pdl_trigger(); return; }
+    const int t0 = u0 / nseg, t1 = (u1 - 1) / nseg + 1;
+    const int row_lo = (t0 / NG) * RB;
+    const int row_hi = min(Wy, ((t1 - 1) / NG + 1) * RB + K - 1);
+    const int g_first = t0 % NG;
+    const int ngr = min(NG, t1 - t0);
+
+    // this warp's unit range, decoded once; then advanced incrementally
+    const int gw = c0 + warp;
+    const int w0 = gw * a.ub + min(gw, a.ur), w1 = (gw + 1) * a.ub + min(gw + 1, a.ur);
+    int t = w0 / nseg, j = w0 - t * nseg;
+    int rb = t / NG, g = t - rb * NG;
+    const int q32 = 32 / L, r32 = 32 - q32 * L;        // slot step of one segment
+    const int rg_l = lane / L, xv_l = lane - rg_l * L;  // slot of this lane in segment 0
+    int rg = rg_l + j * q32, xv = xv_l + j * r32;       // slot of this lane in segment j
+    while (xv >= L) { xv -= L; ++rg; }
+    int gi = g - g_first;
+    if (gi < 0) gi += NG;
+
+    float *s_w = smem;                                // [gmax][GS]
+    float *s_in = smem + a.gmax * GS;                 // input rows [row_lo, row_hi), + pad
+    // s_in[pad + e - e0] = I[e]: smem and global agree mod 16 B
+    const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
+    const int pad = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3);
 
     pdl_wait();
-    // stage taps and the halo band with fire-and-forget cp.async (zero-filled
-    // outside the map), one wait for all of them
-    for (int idx = tid; idx < ngroups * GS; idx += kKsThreads) {
-        const int g = idx / GS, e = idx - g * GS;
+    if (stamp) g_ks_stamps[4 * blockIdx.x + 1] = gtimer();
+    for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
+        const int gi = idx / GS, e = idx - gi * GS;
         const int f = e / KK, t = e - f * KK;
-        const int m = mc0 + g * R + f;
-        const bool ok = f < R && m < mc1;
-        cp_async4(s_w + idx, ok ? F + (int64_t)m * KK + t : F, ok);
+        int g = g_first + gi;
+        if (g >= NG) g -= NG;
+        const int m = g * R + f;
+        const bool ok = f < R && m < M;
+        cp_async4(s_w + idx, ok ? a.F + (int64_t)m * KK + t : a.F, ok);
     }
-    const int hr = rows + K - 1;
-    for (int rr = warp; rr < TY + K - 1; rr += kKsWarps) {
-        const float *src = I + (int64_t)(y0 + rr) * Wx;
-        for (int cc = lane; cc < SW; cc += 32) {
-            const bool ok = rr < hr && cc < Wx;
-            cp_async4(s_in + rr * SW + cc, ok ? src + cc : I, ok);
+    {
+        const int nch = (int)((pad + (e1 - e0) + 3) >> 2);  // 16-B chunks of s_in
+        for (int c = tid; c < nch; c += kKsThreads) {
+            const int64_t e = e0 - pad + 4 * c;            // global element of the chunk's first float
+            if (e >= e0 && e + 4 <= e1) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             ::"r"(smem_u32(s_in + 4 * c)), "l"(a.I + e) : "memory");
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool ok = e + i >= e0 && e + i < e1;
+                    cp_async4(s_in + 4 * c + i, ok ? a.I + e + i : a.I, ok);
+                }
+            }
         }
     }
     cp_async_commit();
     pdl_trigger();
     cp_async_wait<0>();
     __syncthreads();
+    if (stamp) g_ks_stamps[4 * blockIdx.x + 2] = gtimer();
 
-    // lane -> (row within the item, first pixel)
-    int lrow, lx;
-    if (RW > 1) { lrow = lane / Wo; lx = lane - lrow * Wo; }
-    else        { lrow = 0;         lx = lane * TX; }
-    const bool lane_ok = (RW > 1) ? (lrow < RW) : (lx < Wo);
-    const bool lane_full = (RW > 1) || (lx + TX <= Wo);       // no per-pixel bounds checks
+    if (w0 >= w1 && !a.dbg) return;
 
-    const int n_items = n_ri * ngroups;
-    int local = 0;
-    for (int it = warp; it < n_items; it += kKsWarps, ++local) {
-        const int ri = it % n_ri, g = it / n_ri;
-        float *ob = s_out + (local & 1) * R * CHW;
-        if (local >= 2) {
-            if (lane < R) bulk_wait_read<1>();        // this lane's store of 2 items ago read ob
-            __syncwarp();
-        }
-        const int yb = ri * RI;                       // first band row of this item
-        const int nrows = min(RI, rows - yb);         // rows in this item
-        const int len = nrows * Wo;                   // contiguous floats per filter
-        const int m0 = mc0 + g * R;
-        const int64_t g00 = ((int64_t)m0 * Ho + y0 + yb) * Wo;   // range start of filter m0
-        if (lane_ok && lrow < nrows) {
-            float w[GS];
+    const float *sin = s_in + pad - (int64_t)row_lo * Wx;   // sin[y*Wx + x] = I[y][x]
+    const int64_t plane = (int64_t)Ho * Wo;
+    float w[R * KK];
+    bool need_w = true;
+    for (int u = w0; u < w1; ++u) {
+        if (need_w) {                                 // (warp-uniform) new task: load its taps
+            need_w = false;
+            const float *ws = s_w + gi * GS;
 #pragma unroll
-            for (int q = 0; q < GS / 4; ++q) {
-                const float4 v = *reinterpret_cast<const float4 *>(s_w + g * GS + 4 * q);
+            for (int q = 0; q < (R * KK) / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4 *>(ws + 4 * q);
                 w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
             }
-            constexpr int RL = RR;                    // rows computed per lane (1 in small mode)
-            const int nr = (RW > 1) ? 1 : nrows;      // valid rows of this lane's block
-            float acc[RL][R][TX];
 #pragma unroll
-            for (int q = 0; q < RL; ++q)
+            for (int q = (R * KK) & ~3; q < R * KK; ++q) w[q] = ws[q];
+        }
+        const int y0 = rb * RB + rg * RR;
+        const int x = TX * xv;
+        if (rg < a.RWt && y0 < Ho) {
+            float acc[RR][R][TX];
+#pragma unroll
+            for (int q = 0; q < RR; ++q)
 #pragma unroll
                 for (int f = 0; f < R; ++f)
 #pragma unroll
-                    for (int j = 0; j < TX; ++j) acc[q][f][j] = 0.f;
-            const float *base = s_in + (yb + lrow) * SW + lx;
+                    for (int v = 0; v < TX; ++v) acc[q][f][v] = 0.f;
+            const float *base = sin + y0 * Wx + x;
 #pragma unroll
-            for (int ir = 0; ir < RL + K - 1; ++ir) {
-                float win[WN];
+            for (int ir = 0; ir < RR + K - 1; ++ir) {
+                float win[NV * VL];
 #pragma unroll
-                for (int u = 0; u < WN; ++u) win[u] = base[ir * SW + u];
+                for (int i = 0; i < NV; ++i) lds_vec<VL>(base + ir * Wx + i * VL, win + i * VL);
 #pragma unroll
-                for (int q = 0; q < RL; ++q) {
+                for (int q = 0; q < RR; ++q) {
                     const int r = ir - q;             // filter row feeding output row q
                     if (r >= 0 && r < K) {
 #pragma unroll
@@ -139,60 +211,47 @@ ks_kernel(const float *__restrict__ I, int Wx, int Wy, const float *__restrict__
 #pragma unroll
                             for (int f = 0; f < R; ++f)
 #pragma unroll
-                                for (int j = 0; j < TX; ++j)
-                                    acc[q][f][j] = fmaf(win[j + c], w[f * KK + r * K + c], acc[q][f][j]);
+                                for (int v = 0; v < TX; ++v)
+                                    acc[q][f][v] = fmaf(win[v + c], w[f * KK + r * K + c], acc[q][f][v]);
                     }
                 }
             }
-            const int e = lrow * Wo + lx;
+            float *of = a.O + ((int64_t)g * R * Ho + y0) * Wo + x;
+            const int nvs = min(TX, Wo - x);          // valid pixels of this slot (multiple of VS)
+            const int nq = min(RR, Ho - y0), nf = min(R, M - g * R);
 #pragma unroll
-            for (int f = 0; f < R; ++f) {
-                float *d = ob + f * CHW + (int)((g00 + (int64_t)f * plane) & 3) + e;
+            for (int f = 0; f < R; ++f, of += plane) {
+                if (f >= nf) break;
+                float *o = of;
 #pragma unroll
-                for (int q = 0; q < RL; ++q) {
-                    if (q < nr) {
-                        if (lane_full) {
+                for (int q = 0; q < RR; ++q, o += Wo) {
+                    if (q >= nq) break;
 #pragma unroll
-                            for (int j = 0; j < TX; ++j) d[q * Wo + j] = acc[q][f][j];
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < TX; ++j)
-                                if (lx + j < Wo) d[q * Wo + j] = acc[q][f][j];
-                        }
-                    }
+                    for (int v = 0; v < TX; v += VS)
+                        if (TX == VS || v < nvs) stg_vec<VS>(o + v, &acc[q][f][v]);
                 }
             }
         }
-        fence_proxy_async_smem();                     // smem image -> visible to the bulk copy
-        __syncwarp();
-        // lane f < R: bulk store of filter f's 16-B aligned body; all lanes: the
-        // <= 3 head and <= 3 tail elements (or a whole range shorter than 8)
-        if (lane < R) {
-            if (m0 + lane < mc1) {
-                const int64_t g0 = g00 + (int64_t)lane * plane;
-                const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = (g0 + len) & ~(int64_t)3;
-                if (a1 > a0)
-                    bulk_store(O + a0, ob + lane * CHW + (int)(g0 & 3) + (int)(a0 - g0),
-                               (uint32_t)((a1 - a0) * 4));
-            }
-            bulk_commit();
-        }
-        for (int t = lane; t < 8 * R; t += 32) {
-            const int f = t >> 3, j = t & 7;
-            if (m0 + f >= mc1) continue;
-            const int64_t g0 = g00 + (int64_t)f * plane;
-            const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = (g0 + len) & ~(int64_t)3;
-            int64_t gi = -1;
-            if (a1 > a0) {
-                if (j < 4) { if (g0 + j < a0) gi = g0 + j; }
-                else if (a1 + (j - 4) < g0 + len) gi = a1 + (j - 4);
-            } else if (j < len) {
-                gi = g0 + j;
-            }
-            if (gi >= 0) O[gi] = ob[f * CHW + (int)(g0 & 3) + (int)(gi - g0)];
+        // next unit: next segment of this task, or segment 0 of the next task
+        if (++j == nseg) {
+            j = 0;
+            rg = rg_l;
+            xv = xv_l;
+            need_w = true;
+            if (++g == NG) { g = 0; ++rb; }
+            if (++gi == NG) gi = 0;
+        } else {
+            rg += q32;
+            xv += r32;
+            if (xv >= L) { xv -= L; ++rg; }
         }
     }
-    if (lane < R) bulk_wait<0>();                     // keep smem alive until the copies finish
+    if (a.dbg) {
+        __syncthreads();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (stamp) g_ks_stamps[4 * blockIdx.x + 3] = (gtimer() << 8) | smid;
+    }
 }
 
 // Generic fallback (any K, e.g. K = Wx = Wy, or rows too wide for smem): no
@@ -232,20 +291,99 @@ ks_kernel_generic(const float *__restrict__ I, int Wx, int Wy, const float *__re
 }
 
 namespace {
-constexpr int kKsMaxSmem = 110 * 1024;
 
-// (R filters, RR rows) per lane and item: K=1 store-bound -> more filters;
-// K>=5 FMA-bound -> more rows (an input row feeds min(RR, K) output rows)
-__host__ __device__ constexpr int ks_R(int K) { return K <= 1 ? 4 : (K <= 5 ? 2 : 1); }
-__host__ __device__ constexpr int ks_RR(int K) { return K <= 1 ? 1 : (K <= 5 ? 2 : 4); }
-int ks_TX(int Wo) { return (Wo + 31) / 32; }
-int ks_smem(int K, int R, int TX, int TY, int Wx, int Wo, int m_per) {
-    const int RW = (TX == 1 && Wo <= 16) ? 32 / Wo : 1;
-    const int RI = RW > 1 ? RW : ks_RR(K);
-    const int SW = ((RW > 1 ? Wx : 32 * TX + K - 1) + 3) & ~3;
-    const int GS = (R * K * K + 3) & ~3;
-    const int CHW = ((RI * Wo + 3) & ~3) + 4;
-    return (((m_per + R - 1) / R) * GS + (TY + K - 1) * SW + kKsWarps * 2 * R * CHW) * 4;
+// per lane: TX pixels x RR rows x R filters.  K = 1 is store-bound -> many
+// filters; large K is FMA-bound -> 4 pixels x 4 rows (an input row feeds
+// min(RR, K) outputs, a window row of TX+K-1 loads feeds TX*K FMAs per filter)
+__host__ __device__ constexpr int ks_TX(int K) { return K == 1 ? 4 : (K <= 3 ? 2 : 4); }
+__host__ __device__ constexpr int ks_R(int K) { return K <= 1 ? 8 : (K <= 3 ? 4 : 1); }
+__host__ __device__ constexpr int ks_RR(int K) { return K <= 1 ? 1 : (K <= 3 ? 2 : 4); }
+
+struct KsPlan {
+    KsArgs a;
+    int VL, VS, G, smem;
+};
+
+bool al(const void *p, int bytes) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % bytes == 0; }
+
+// Max dynamic smem over the CTAs of a grid of G CTAs (filter taps + input rows).
+void ks_cta_needs(const KsArgs &a, int K, int R, int RR, int TX, int G, int *gmax, int *smem) {
+    const int KK = K * K, GS = (R * KK + 3) & ~3, RB = a.RWt * RR;
+    int rows_max = 0, g = 1;
+    for (int c = 0; c < G; ++c) {
+        const int c0 = c * kKsWarps, c1 = c0 + kKsWarps;
+        const int u0 = c0 * a.ub + (c0 < a.ur ? c0 : a.ur), u1 = c1 * a.ub + (c1 < a.ur ? c1 : a.ur);
+        if (u0 >= u1) continue;
+        const int t0 = u0 / a.nseg, t1 = (u1 - 1) / a.nseg + 1;
+        const int n = t1 - t0 < a.NG ? t1 - t0 : a.NG;
+        const int rows = ((t1 - 1) / a.NG - t0 / a.NG + 1) * RB + K - 1;
+        if (n > g) g = n;
+        if (rows > rows_max) rows_max = rows;
+    }
+    *gmax = g;
+    *smem = (g * GS + rows_max * a.Wx + 2 * TX + 8) * 4;
+}
+
+// Returns false when the band kernel does not apply (K > 7 or the staged rows
+// of a CTA do not fit in shared memory).
+bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O, KsPlan *kp) {
+    if (K > 7) return false;
+    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
+    const int TX = ks_TX(K), R = ks_R(K), RR = ks_RR(K);
+    KsArgs a = {};
+    a.I = I; a.F = F; a.O = O;
+    a.Wx = Wx; a.Wy = Wy; a.M = M;
+    a.L = (Wo + TX - 1) / TX;
+    // row groups per task: fewest lane-steps per filter group,
+    //   ceil(Ho / (RWt*RR)) row blocks x ceil(RWt*L / 32) segments
+    // (within 5 % of the minimum, the shortest task: finer work ranges and
+    // fewer staged rows; two row blocks of input must fit in ~40 KB)
+    int64_t cost[33];
+    int64_t best = -1;
+    int nr = 0;
+    for (int rwt = 1; rwt <= 32; ++rwt) {
+        if (rwt > 1 && (int64_t)(rwt - 1) * RR >= Ho) break;      // taller than the map
+        if (rwt > 1 && (int64_t)(2 * rwt * RR + K - 1) * Wx * 4 > 40 * 1024) break;
+        cost[rwt] = (int64_t)((Ho + rwt * RR - 1) / (rwt * RR)) * ((rwt * a.L + 31) / 32);
+        if (best < 0 || cost[rwt] < best) best = cost[rwt];
+        nr = rwt;
+    }
+    a.RWt = 1;
+    for (int rwt = 1; rwt <= nr; ++rwt)
+        if (cost[rwt] * 100 <= best * 105) { a.RWt = rwt; break; }
+    a.NG = (M + R - 1) / R;
+    a.nseg = (a.RWt * a.L + 31) / 32;
+    const int64_t NRB = (Ho + a.RWt * RR - 1) / (a.RWt * RR);
+    const int64_t U = NRB * a.NG * a.nseg;
+    if (U > (int64_t)1 << 30) return false;
+    a.U = (int)U;
+    // one wave of ks_min_blocks(K) CTAs per SM, or one unit per warp if fewer
+    const int cap = ks_min_blocks(K) * kNumSMs;
+    const int max_smem = (ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
+    int G = (a.U + kKsWarps - 1) / kKsWarps;
+    if (G > cap) G = cap;
+    if (const char *e = getenv("B200CONV_KS_G")) {        // experiments: CTA count override
+        const int g = atoi(e);
+        if (g > 0) G = g < a.U ? g : a.U;
+    }
+    for (;;) {
+        a.NW = G * kKsWarps;
+        a.ub = a.U / a.NW;
+        a.ur = a.U - a.ub * a.NW;
+        int smem;
+        ks_cta_needs(a, K, R, RR, TX, G, &a.gmax, &smem);
+        if (smem <= max_smem || G >= a.U) {
+            if (smem > 200 * 1024) return false;
+            kp->a = a;
+            kp->VL = (Wx % TX == 0 && al(I, 4 * TX)) ? TX : 1;
+            kp->VS = (Wo % TX == 0 && al(O, 4 * TX)) ? TX : ((TX >= 2 && Wo % 2 == 0 && al(O, 8)) ? 2 : 1);
+            kp->G = G;
+            kp->smem = smem;
+            return true;
+        }
+        if (G >= 4 * cap) return false;
+        G = G * 2 > a.U ? a.U : G * 2;               // finer ranges -> fewer rows per CTA
+    }
 }
 }  // namespace
 
@@ -254,40 +392,22 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
     p->cluster_x = 1;
     p->tma_f = 0;
     p->launches = 1;
-    const int TX = ks_TX(Wo);
-    if (K <= 7 && TX <= 8) {
-        const int R = ks_R(K);
-        // (band rows TY, filters per CTA m_per): minimise waves x work per CTA on
-        // 148 SMs x 2 CTAs (+ a per-CTA staging cost), i.e. avoid a ragged last wave
-        const int slots = 2 * kNumSMs;
-        int TY = Ho < 16 ? Ho : 16, m_per = R;
-        double best = -1.0;
-        for (int ty : {8, 16}) {
-            const int t = Ho < ty ? Ho : ty;
-            const int nb = (Ho + t - 1) / t;
-            for (int mp = R; mp < M + R; mp += R) {
-                const int ctas = nb * ((M + mp - 1) / mp);
-                const int waves = (ctas + slots - 1) / slots;
-                const double cost = waves * ((double)t * mp + 4.0 * (t + K - 1));
-                if (best < 0 || cost < best - 1e-9) { best = cost; TY = t; m_per = mp; }
-                if (ctas <= slots) break;                 // larger chunks only lengthen the wave
-            }
-            if (Ho <= ty) break;
-        }
-        const int bands = (Ho + TY - 1) / TY;
-        p->kernel = 0;
+    p->kernel = 0;
+    KsPlan kp;
+    // plans are computed for 16-B aligned I / O (torch allocations)
+    if (plan_ks(reinterpret_cast<const float *>(256), Wx, Wy, nullptr, K, M,
+                reinterpret_cast<float *>(256), &kp)) {
         p->block_x = kKsThreads;
-        p->grid_x = (M + m_per - 1) / m_per;
-        p->grid_y = bands;
+        p->grid_x = kp.G;
+        p->grid_y = 1;
         p->grid_z = 1;
-        p->tile_m = m_per;                               // filters per CTA (groups of R)
-        p->tile_n = TY;                                  // output rows per CTA band (full width)
-        p->smem_bytes = ks_smem(K, R, TX, TY, Wx, Wo, m_per);
-        if (p->smem_bytes <= kKsMaxSmem) return 0;
+        p->tile_m = ks_R(K);                              // filters per task
+        p->tile_n = kp.a.RWt * ks_RR(K);                  // output rows per task (full width)
+        p->smem_bytes = kp.smem;
+        return 0;
     }
     // generic fallback: (x, y, m) tiles of 1 column x 4 rows x 4 filters per thread
     const int bx = Wo >= 128 ? 128 : ((Wo + 31) / 32) * 32;
-    p->kernel = 0;
     p->block_x = bx;
     p->grid_x = (Wo + bx - 1) / bx;
     p->grid_y = (Ho + 3) / 4;
@@ -305,60 +425,62 @@ static cudaLaunchAttribute pdl_attr() {
     return a;
 }
 
-template <int K, int TX>
-static cudaError_t launch_ks(const conv_plan &p, const float *I, int Wx, int Wy, const float *F,
-                             int M, float *O, cudaStream_t s) {
-    auto kern = ks_kernel<K, ks_R(K), TX, ks_RR(K)>;
-    if (p.smem_bytes > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p.smem_bytes);
+template <int K, int VL, int VS>
+static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
+    auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R(K), ks_RR(K)>;
+    if (kp.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.smem);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
-    cfg.blockDim = dim3(p.block_x);
-    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.gridDim = dim3(kp.G);
+    cfg.blockDim = dim3(kKsThreads);
+    cfg.dynamicSmemBytes = kp.smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1] = {pdl_attr()};
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, I, Wx, Wy, F, M, O, p.tile_m, p.tile_n);
+    KsArgs a = kp.a;
+    const char *dbg = getenv("B200CONV_KS_DBG");
+    a.dbg = dbg ? atoi(dbg) : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// VL in {TX, 1}; VS in {TX, 2, 1} (2 only when TX = 4)
 template <int K>
-static cudaError_t launch_ks_v(const conv_plan &p, const float *I, int Wx, int Wy, const float *F,
-                               int M, float *O, cudaStream_t s) {
-    switch (ks_TX(Wx - K + 1)) {
-        case 1: return launch_ks<K, 1>(p, I, Wx, Wy, F, M, O, s);
-        case 2: return launch_ks<K, 2>(p, I, Wx, Wy, F, M, O, s);
-        case 3: return launch_ks<K, 3>(p, I, Wx, Wy, F, M, O, s);
-        case 4: return launch_ks<K, 4>(p, I, Wx, Wy, F, M, O, s);
-        case 5: return launch_ks<K, 5>(p, I, Wx, Wy, F, M, O, s);
-        case 6: return launch_ks<K, 6>(p, I, Wx, Wy, F, M, O, s);
-        case 7: return launch_ks<K, 7>(p, I, Wx, Wy, F, M, O, s);
-        default: return launch_ks<K, 8>(p, I, Wx, Wy, F, M, O, s);
+static cudaError_t launch_ks_v(const KsPlan &kp, cudaStream_t s) {
+    constexpr int TX = ks_TX(K);
+    constexpr int V2 = TX >= 2 ? 2 : 1;
+    if (kp.VL == TX) {
+        if (kp.VS == TX) return launch_ks<K, TX, TX>(kp, s);
+        if (kp.VS == 2) return launch_ks<K, TX, V2>(kp, s);
+        return launch_ks<K, TX, 1>(kp, s);
     }
+    if (kp.VS == TX) return launch_ks<K, 1, TX>(kp, s);
+    if (kp.VS == 2) return launch_ks<K, 1, V2>(kp, s);
+    return launch_ks<K, 1, 1>(kp, s);
 }
 
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                           cudaStream_t s) {
-    conv_plan p;
-    plan_single(Wx, Wy, K, M, &p);
-    if (p.tile_n > 0) {
+    KsPlan kp;
+    if (plan_ks(I, Wx, Wy, F, K, M, O, &kp)) {
         switch (K) {
-            case 1: return launch_ks_v<1>(p, I, Wx, Wy, F, M, O, s);
-            case 2: return launch_ks_v<2>(p, I, Wx, Wy, F, M, O, s);
-            case 3: return launch_ks_v<3>(p, I, Wx, Wy, F, M, O, s);
-            case 4: return launch_ks_v<4>(p, I, Wx, Wy, F, M, O, s);
-            case 5: return launch_ks_v<5>(p, I, Wx, Wy, F, M, O, s);
-            case 6: return launch_ks_v<6>(p, I, Wx, Wy, F, M, O, s);
-            case 7: return launch_ks_v<7>(p, I, Wx, Wy, F, M, O, s);
+            case 1: return launch_ks_v<1>(kp, s);
+            case 2: return launch_ks_v<2>(kp, s);
+            case 3: return launch_ks_v<3>(kp, s);
+            case 4: return launch_ks_v<4>(kp, s);
+            case 5: return launch_ks_v<5>(kp, s);
+            case 6: return launch_ks_v<6>(kp, s);
+            case 7: return launch_ks_v<7>(kp, s);
             default: break;
         }
     }
+    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
+    const int bx = Wo >= 128 ? 128 : ((Wo + 31) / 32) * 32;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
-    cfg.blockDim = dim3(p.block_x);
+    cfg.gridDim = dim3((Wo + bx - 1) / bx, (Ho + 3) / 4, (M + 3) / 4);
+    cfg.blockDim = dim3(bx);
     cfg.stream = s;
     cudaLaunchAttribute attr[1] = {pdl_attr()};
     cfg.attrs = attr;

@@ -88,8 +88,11 @@ def test_plans_cover_every_config_with_one_launch():
         assert p["kernel"] == 0 and p["grid_x"] * p["grid_y"] * p["grid_z"] >= 1
         Ho, Wo = cfg["Wy"] - cfg["K"] + 1, cfg["Wx"] - cfg["K"] + 1
         assert p["tile_n"] > 0, "every BASELINE single-channel config uses the band kernel"
-        assert p["grid_x"] * p["tile_m"] >= cfg["M"]          # filter chunks
-        assert p["grid_y"] * p["tile_n"] >= Ho                # full-width row bands
+        # tasks = (row block of tile_n full-width rows) x (group of tile_m filters),
+        # dealt to at most one wave of 3 CTAs per SM, at most one 32-slot segment per warp
+        assert p["grid_y"] == p["grid_z"] == 1 and 1 <= p["grid_x"] <= 3 * 148
+        tasks = -(-Ho // p["tile_n"]) * -(-cfg["M"] // p["tile_m"])
+        assert p["grid_x"] * 8 <= tasks * -(-(p["tile_n"] * Wo) // 32) or p["grid_x"] == 1
         assert p["smem_bytes"] <= 227 * 1024
     for cfg in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
         for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
