@@ -287,11 +287,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         const int m = mlo + idx / BQ, n = 4 * (idx % BQ);
         float4 v;
         if (S > 1) {
-            v = ld_dsmem_f32x4(mapa_shared(Pbase + (m * BN + n) * 4, 0));
-            for (int t = 1; t < S; ++t) {
-                const float4 u = ld_dsmem_f32x4(mapa_shared(Pbase + (m * BN + n) * 4, t));
-                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
-            }
+            v = dsmem_sum_ranks<kSimtMaxSplit>(Pbase + (m * BN + n) * 4, S);
         } else {
             v = *reinterpret_cast<const float4 *>(P + m * BN + n);
         }

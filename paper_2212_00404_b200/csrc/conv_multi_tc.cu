@@ -105,15 +105,29 @@ __device__ __forceinline__ uint32_t sw128_off(int g, int j) {
 
 __device__ unsigned long long g_tc_stamps[1024];   // diagnostics (dbg & 128)
 
+// dbg & 256: per-CTA timeline, globaltimer ns: [start, after griddepcontrol.wait,
+// first k-block ready (MMA warp), last MMA retired (tmem_full), partial/epilogue
+// done, end (after the cluster reduction) << 8 | smid], CTAs 0..1023 (linear id)
+__device__ unsigned long long g_tc_cta[8 * 1024];
+
 int tc_read_stamps(unsigned long long *host) {
     return cudaMemcpyFromSymbol(host, g_tc_stamps, sizeof(g_tc_stamps)) == cudaSuccess ? 0 : 1;
+}
+int tc_read_cta_stamps(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_tc_cta, sizeof(g_tc_cta)) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ unsigned long long tc_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 __global__ void __launch_bounds__(kTcThreads, 1)
 kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
             const void *__restrict__ Iv, const void *__restrict__ Fv, int C, int Wx, int Wy,
-            int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg) {
+            int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg,
+            float *__restrict__ Wk) {
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
     constexpr int BK = Tr::kBK;
@@ -135,6 +149,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
 
     const int S = gridDim.x;
     const int split = blockIdx.x;
+    const int tile_lin = blockIdx.y + gridDim.y * blockIdx.z;
     const int p0 = blockIdx.y * kTcBM;
     const int n0 = blockIdx.z * BN;
     const int kb0 = split * kb_per_split;
@@ -149,6 +164,8 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     uint64_t *empty = pfull + kTcMaxStages;                              // MMA done with stage
     uint64_t *tmem_full = empty + kTcMaxStages;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    uint64_t *red_bar = tmem_full + 2;                                   // split-K slices landed
+    float *P = reinterpret_cast<float *>(smem);      // [BN][128] partial tile (split > 1), aliases the stages
     int *ktab = reinterpret_cast<int *>(smem + NS * STAGE + 512);        // [K*K][BK]
     const bool use_tab = kPatch && patch2d && geo.tab_bytes > 0;
     if (use_tab) {
@@ -161,6 +178,9 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool tl = (dbg & 256) && cta_lin < 1024;
+    if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin] = tc_gtimer();
     // dbg & 128: CTA (0,0,0) records globaltimer stamps per iteration into O
     //   O[i] producer issue, O[256+i] gather(warp 2) arrive, O[512+i] MMA commit
     const bool stamp = (dbg & 128) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
@@ -176,6 +196,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
             mbar_init(&empty[s], 1);                    // tcgen05.commit
         }
         mbar_init(tmem_full, 1);
+        mbar_init(red_bar, 1);
         fence_mbar_init();
         if (kTmaB) tma_prefetch_desc(&tmapF);
         if (kPatch) tma_prefetch_desc(&tmapI);
@@ -187,6 +208,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     const uint32_t tmem = *tmem_slot;
     pdl_wait();                     // prologue above overlaps the previous kernel's tail
     pdl_trigger();
+    if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 1] = tc_gtimer();
 
     if (warp >= kProdWarp && warp < kMmaWarp) {
         // ------------------------------------------------ TMA producer
@@ -249,6 +271,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                 const int s = i % NS;
                 wait(&full[s], (i / NS) & 1);
                 tc_fence_after();
+                if (tl && i == 0) g_tc_cta[8 * cta_lin + 2] = tc_gtimer();
                 const uint32_t a_addr = smem_u32(smem + s * STAGE);
                 const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
@@ -409,11 +432,11 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
         const bool valid = (pe < Ho * Wx) && (x < Wo);
         const int64_t obase = (int64_t)y * Wo + x;
         const int64_t plane = (int64_t)Ho * Wo;
-        float *P = reinterpret_cast<float *>(smem);      // [BN][128] partial tile (split > 1)
         if (niter > 0) {
             mbar_wait(tmem_full, 0);
             tc_fence_after();
         }
+        if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 3] = tc_gtimer();
         constexpr int NCB = BN / 32;                     // 32-column blocks
         for (int cb = half; cb < NCB; cb += 2) {
             uint32_t r[32];
@@ -437,28 +460,62 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                 for (int j = 0; j < 32; ++j) P[(cb * 32 + j) * kTcBM + row] = __uint_as_float(r[j]);
             }
         }
+        if (S > 1 && Wk) fence_proxy_async_smem();       // P -> visible to the bulk store
         tc_fence_before();
     }
 
     __syncthreads();
+    if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 4] = tc_gtimer();
     if (S > 1) {
-        // ---------------------------------------------- split-K reduce via DSMEM
+        // ---------------------------------------------- split-K reduce
+        // L2 path: the partial tile leaves in ONE bulk store to the workspace
+        // [split][tile][BN][128]; after the cluster barrier each rank bulk-loads
+        // its filter rows of all S partials into (the now free) smem and sums
+        // them in rank order.  DSMEM path (no workspace): sums the ranks' smem
+        // tiles directly.
+        if (Wk && threadIdx.x == 0) {
+            float *wmine = Wk + ((int64_t)split * gridDim.y * gridDim.z + tile_lin) * BN * kTcBM;
+            bulk_store(wmine, P, (uint32_t)(BN * kTcBM * 4));
+            bulk_commit();
+            bulk_wait<0>();
+            fence_proxy_async_global();
+        }
         cluster_sync_all();
+        if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 6] = tc_gtimer();
         const int nlo = split * BN / S;                  // filters [nlo, nhi) owned by this rank
         const int rows = (split + 1) * BN / S - nlo;
         const uint32_t Pbase = smem_u32(smem);
         const int64_t plane = (int64_t)Ho * Wo;
-        // 4 pixels per thread: 16-B DSMEM loads from every rank, summed in rank order
+        // 4 pixels per thread: 16-B loads of every rank's partial (L2 workspace
+        // or DSMEM), all in flight at once, summed in rank order
+        float *slices = P;                               // [S][rows][128]
+        if (Wk) {
+            if (threadIdx.x == 0) {
+                const int64_t wslice = (int64_t)gridDim.y * gridDim.z * BN * kTcBM;
+                const float *wt = Wk + ((int64_t)tile_lin * BN + nlo) * kTcBM;
+                const uint32_t bytes = (uint32_t)(rows * kTcBM * 4);
+                mbar_arrive_expect_tx(red_bar, bytes * S);
+                for (int t = 0; t < S; ++t) bulk_load(slices + t * rows * kTcBM, wt + t * wslice, bytes, red_bar);
+            }
+            mbar_wait(red_bar, 0);
+        }
         for (int idx = threadIdx.x; idx < rows * (kTcBM / 4); idx += kTcThreads) {
             const int nl = nlo + idx / (kTcBM / 4), row0 = 4 * (idx % (kTcBM / 4));
             const uint32_t off = (uint32_t)((nl * kTcBM + row0) * 4);
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int t = 0; t < S; ++t) {
-                const float4 u = ld_dsmem_f32x4(mapa_shared(Pbase + off, (uint32_t)t));
-                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+            if (dbg & 512) {
+            } else if (Wk) {
+                const float *sl = slices + (nl - nlo) * kTcBM + row0;
+                v = *reinterpret_cast<const float4 *>(sl);
+                for (int t = 1; t < S; ++t) {
+                    const float4 u = *reinterpret_cast<const float4 *>(sl + t * rows * kTcBM);
+                    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+                }
+            } else {
+                v = dsmem_sum_ranks<kTcMaxSplit>(Pbase + off, S);
             }
             const int m = n0 + nl;
-            if (m < M) {
+            if (m < M && !(dbg & 1024)) {
                 const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -468,7 +525,12 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                 }
             }
         }
-        cluster_sync_all();
+        if (!Wk) cluster_sync_all();          // keep this CTA's partial alive for the others
+    }
+    if (tl && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_tc_cta[8 * cta_lin + 5] = (tc_gtimer() << 8) | smid;
     }
     if (warp == kMmaWarp) {
         tc_fence_after();
@@ -564,7 +626,15 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
     cfg.numAttrs = 2;
     const char *dbgs = getenv("B200CONV_TC_DBG");
     const int dbg = dbgs ? atoi(dbgs) : 0;
-    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg);
+    // split-K partials go through the L2 workspace (DSMEM reduction when the
+    // workspace cannot grow during stream capture, or with B200CONV_TC_DSMEM=1)
+    float *Wk = nullptr;
+    const char *dsm = getenv("B200CONV_TC_DSMEM");
+    if (p.cluster_x > 1 && !(dsm && dsm[0] == '1')) {
+        const size_t bytes = (size_t)p.cluster_x * p.grid_y * p.grid_z * BN * kTcBM * 4;
+        Wk = static_cast<float *>(workspace_get(bytes, s));
+    }
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg, Wk);
 }
 
 template <bool kTF32, int BN>

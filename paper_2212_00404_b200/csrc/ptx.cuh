@@ -173,6 +173,23 @@ __device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t cluster_addr) {
     return v;
 }
 
+// Sum of the float4 at the same smem offset in cluster ranks 0..S-1 (S <= MAXS),
+// added in rank order (deterministic).  All S distributed-shared loads are
+// issued before the first add, so the reduction costs one DSMEM round trip,
+// not S of them.
+template <int MAXS>
+__device__ __forceinline__ float4 dsmem_sum_ranks(uint32_t local_addr, int S) {
+    float4 u[MAXS];
+#pragma unroll
+    for (int t = 0; t < MAXS; ++t)
+        if (t < S) u[t] = ld_dsmem_f32x4(mapa_shared(local_addr, (uint32_t)t));
+    float4 v = u[0];
+#pragma unroll
+    for (int t = 1; t < MAXS; ++t)
+        if (t < S) { v.x += u[t].x; v.y += u[t].y; v.z += u[t].z; v.w += u[t].w; }
+    return v;
+}
+
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 __device__ __forceinline__ void cp_async4(void *dst, const void *src, bool pred) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
@@ -187,6 +204,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  ::"l"(reinterpret_cast<uint64_t>(gdst)), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+// global -> smem 1-D bulk copy completing on an mbarrier (complete_tx bytes).
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(sdst)), "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>

@@ -11,14 +11,16 @@
 // O[M][Ho*Wo].
 //
 // The workspace is owned by the library: one buffer per (device, stream),
-// grown (never shrunk) on demand outside stream capture; a call made while
-// the stream is being captured that would need a bigger buffer gets nullptr
-// and the caller falls back to a cluster-only plan.
+// grown (never shrunk, old buffers retired but kept alive) on demand outside
+// stream capture; a call made while the stream is being captured that would
+// need a bigger buffer gets nullptr and the caller falls back to a plan that
+// needs none (cluster / DSMEM reduction).
 #include <cstdint>
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -28,6 +30,7 @@ namespace {
 struct WsBuf { void *p = nullptr; size_t bytes = 0; };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
+std::vector<void *> g_ws_retired;
 }  // namespace
 
 void *workspace_get(size_t bytes, cudaStream_t s) {
@@ -39,14 +42,16 @@ void *workspace_get(size_t bytes, cudaStream_t s) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) { cudaGetLastError(); return nullptr; }
     if (cs != cudaStreamCaptureStatusNone) return nullptr;
-    // in-flight work on this stream may still read the old buffer
+    // The old buffer is retired, not freed: in-flight work, or a CUDA graph
+    // captured earlier on this stream, may still reference it.  Growth is
+    // geometric, so retired buffers total less than the live one.
     if (b.p) {
-        if (cudaStreamSynchronize(s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-        cudaFree(b.p);
+        g_ws_retired.push_back(b.p);
         b.p = nullptr;
-        b.bytes = 0;
     }
     size_t want = bytes < (size_t(16) << 20) ? (size_t(16) << 20) : bytes;
+    if (want < 2 * b.bytes) want = 2 * b.bytes;
+    b.bytes = 0;
     if (cudaMalloc(&b.p, want) != cudaSuccess) { cudaGetLastError(); b.p = nullptr; return nullptr; }
     b.bytes = want;
     return b.p;

@@ -5,9 +5,11 @@ from paper_2212_00404_b200 import conv
 dbg = sys.argv[1]
 os.environ['B200CONV_TC_DBG'] = dbg
 dev = torch.device('cuda', 0)
-for (C, W, K, M, prec) in [(512, 14, 3, 4096, 'tf32'), (256, 28, 3, 256, 'tf32')]:
-    I = torch.from_numpy(synth.uniform01(1, (C, W, W))).to(dev)
-    F = torch.from_numpy(synth.uniform_pm1(2, (M, C, K, K))).to(dev)
+LAYERS = [tuple(int(v) if v.isdigit() else v for v in a.split(',')) for a in sys.argv[2:]] or [(512, 14, 3, 4096, 'tf32'), (256, 28, 3, 256, 'tf32')]
+for (C, W, K, M, prec) in LAYERS:
+    dt = torch.bfloat16 if prec == 'bf16' else torch.float32
+    I = torch.from_numpy(synth.uniform01(1, (C, W, W))).to(dev, dt)
+    F = torch.from_numpy(synth.uniform_pm1(2, (M, C, K, K))).to(dev, dt)
     O = torch.zeros((M, W - K + 1, W - K + 1), device=dev)
     for _ in range(3):
         conv.conv_multi_ex(I, C, W, W, F, K, M, O, prec)
