@@ -202,19 +202,21 @@ ks_kernel(const KsArgs a) {
                 float win[NV * VL];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) lds_vec<VL>(base + ir * Wx + i * VL, win + i * VL);
+                // c outermost: consecutive FMAs update RR*R*TX different
+                // accumulators (a lone warp on an SMSP stays at full issue rate)
 #pragma unroll
-                for (int q = 0; q < RR; ++q) {
-                    const int r = ir - q;             // filter row feeding output row q
-                    if (r >= 0 && r < K) {
+                for (int c = 0; c < K; ++c)
 #pragma unroll
-                        for (int c = 0; c < K; ++c)
+                    for (int q = 0; q < RR; ++q) {
+                        const int r = ir - q;         // filter row feeding output row q
+                        if (r >= 0 && r < K) {
 #pragma unroll
                             for (int f = 0; f < R; ++f)
 #pragma unroll
                                 for (int v = 0; v < TX; ++v)
                                     acc[q][f][v] = fmaf(win[v + c], w[f * KK + r * K + c], acc[q][f][v]);
+                        }
                     }
-                }
             }
             float *of = a.O + ((int64_t)g * R * Ho + y0) * Wo + x;
             const int nvs = min(TX, Wo - x);          // valid pixels of this slot (multiple of VS)
@@ -358,7 +360,10 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
     if (U > (int64_t)1 << 30) return false;
     a.U = (int)U;
     // one wave of ks_min_blocks(K) CTAs per SM, or one unit per warp if fewer
-    const int cap = ks_min_blocks(K) * kNumSMs;
+    // (K = 1, pure store stream: one CTA per SM measured fastest — 9.4 vs
+    // 11.5 us for 224x224 M=256 — fewer warps per SM keep the store traffic
+    // fairer across SMs; see tools/ks_variants.py)
+    const int cap = (K == 1 ? 1 : ks_min_blocks(K)) * kNumSMs;
     const int max_smem = (ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
     int G = (a.U + kKsWarps - 1) / kKsWarps;
     if (G > cap) G = cap;
