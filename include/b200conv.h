@@ -117,14 +117,16 @@ B200CONV_API int conv_multi_host(const void *I, int C, int Wx, int Wy, const voi
  * the channel split is reduced through the library's split-K workspace
  * (launches == 2: a deterministic fixed-order reduction kernel follows). */
 typedef struct {
-    int kernel;        /* 0 = KS (single FP32), 1 = KM-SIMT (multi FP32), 2 = KM-TC (tf32/bf16) */
+    int kernel;        /* 0 = KS (single FP32), 1 = KM-SIMT (multi FP32), 2 = KM-TC implicit (tf32/bf16),
+                          3 = KM-TC/G: im2col kernel + TMA-fed tcgen05 GEMM (tf32/bf16) */
     int grid_x, grid_y, grid_z;
     int block_x;
     int cluster_x;     /* split-K factor over channels / K-blocks (1 = none) */
     int tile_m;        /* filters per CTA tile */
     int tile_n;        /* (wide) output pixels per CTA tile */
     int smem_bytes;    /* dynamic shared memory per CTA */
-    int tma_f;         /* bit 0: F tiles by TMA; bit 1: I patch by TMA (KM-TC) */
+    int tma_f;         /* bit 0: F tiles by TMA; bit 1: I patch by TMA (KM-TC); bit 2: im2col tiles by
+                          TMA (KM-TC/G); bit 3: filters on the 128-lane M side (KM-TC/G) */
     int launches;      /* kernel launches per call: 1, or 2 (split-K through the workspace;
                           cluster_x is then 1 and grid_x is the split count) */
 } conv_plan;

@@ -87,9 +87,15 @@ int run_multi(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
             return launch_status(launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy,
                                                    static_cast<const float *>(F), K, M, O, s));
         case CONV_TF32:
-            return launch_status(launch_multi_tc(I, C, Wx, Wy, F, K, M, O, false, s));
-        case CONV_BF16:
-            return launch_status(launch_multi_tc(I, C, Wx, Wy, F, K, M, O, true, s));
+        case CONV_BF16: {
+            const bool bf16 = precision == CONV_BF16;
+            cudaError_t e = launch_multi_gemm(I, C, Wx, Wy, F, K, M, O, bf16, s);
+            if (e == cudaErrorNotSupported) {   // shape / alignment / capture: implicit kernel
+                cudaGetLastError();
+                e = launch_multi_tc(I, C, Wx, Wy, F, K, M, O, bf16, s);
+            }
+            return launch_status(e);
+        }
         default:
             return CONV_E_PRECISION;
     }
@@ -233,8 +239,14 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
     if (!out) return CONV_E_NULL;
     switch (precision) {
         case CONV_FP32: plan_multi_simt(C, Wx, Wy, K, M, out); return CONV_OK;
-        case CONV_TF32: plan_multi_tc(C, Wx, Wy, K, M, false, nullptr, out); return CONV_OK;
-        case CONV_BF16: plan_multi_tc(C, Wx, Wy, K, M, true, nullptr, out); return CONV_OK;
+        case CONV_TF32:
+        case CONV_BF16: {
+            const bool bf16 = precision == CONV_BF16;
+            const char *gm = getenv("B200CONV_GM");
+            if ((gm && gm[0] == '0') || plan_multi_gemm(C, Wx, Wy, K, M, bf16, out) != 0)
+                plan_multi_tc(C, Wx, Wy, K, M, bf16, nullptr, out);
+            return CONV_OK;
+        }
         default: return CONV_E_PRECISION;
     }
 }

@@ -28,6 +28,13 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
 cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
                             float *O, bool bf16, cudaStream_t s);
 
+// KM-TC/G: explicit im2col (L2-resident workspace) + TMA-fed tcgen05 GEMM
+// (conv_multi_gemm.cu).  plan returns nonzero / launch returns
+// cudaErrorNotSupported when the shape, alignment or workspace rules it out.
+int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *p);
+cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                              bool bf16, cudaStream_t s);
+
 // Split-K chooser: cluster size S (1..max_split) minimising
 //   waves(S) * ceil(units / S) * t_unit + (S > 1) * t_reduce,
 // waves(S) = ceil(tiles / clusters_resident(S)), with the co-resident cluster

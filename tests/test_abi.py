@@ -95,10 +95,16 @@ def test_plans_cover_every_config_with_one_launch():
         assert p["grid_x"] * 8 <= tasks * -(-(p["tile_n"] * Wo) // 32) or p["grid_x"] == 1
         assert p["smem_bytes"] <= 227 * 1024
     for cfg in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
-        for prec, kern in (("fp32", 1), ("tf32", 2), ("bf16", 2)):
+        for prec, kern in (("fp32", (1,)), ("tf32", (2, 3)), ("bf16", (2, 3))):
             p = conv.plan_multi(cfg["C"], cfg["Wx"], cfg["Wy"], cfg["K"], cfg["M"], prec)
-            assert p["kernel"] == kern
+            assert p["kernel"] in kern
             assert 1 <= p["cluster_x"] <= 16 and p["launches"] in (1, 2)
+            if p["kernel"] == 3:
+                # im2col kernel + GEMM; k split reduced inside a cluster
+                assert p["launches"] == 2 and p["grid_x"] == p["cluster_x"] and p["tma_f"] & 5 == 5
+                aligned = (cfg["C"] * cfg["K"] ** 2 * (2 if prec == "bf16" else 4)) % 16 == 0
+                assert aligned, "KM-TC/G needs TMA-able filter rows"
+                continue
             if p["launches"] == 1:
                 assert p["grid_x"] == p["cluster_x"]           # split reduced inside a cluster
             else:

@@ -251,3 +251,44 @@ def test_sharded_multi_virtual_ranks(conv):
         torch.cuda.synchronize()
         Og = torch.cat(parts).cpu().numpy().astype(np.float64)
         assert_parity(Og, Oo, A, TAU[prec], f"virtual shards {prec}")
+
+
+# KM-TC has two tensor-core paths: the im2col + TMA GEMM pair (KM-TC/G, the
+# planner's choice for few-pixel, many-filter layers; B200CONV_GM=2 forces it
+# wherever filter rows are TMA-able) and the implicit kernel (everything else,
+# and the fallback when no workspace can be had during stream capture).
+# Both are covered explicitly, with the split-K variants each one can take.
+TC_PATHS = {
+    "implicit": {"B200CONV_GM": "0"},
+    "implicit-dsmem": {"B200CONV_GM": "0", "B200CONV_TC_DSMEM": "1"},
+    "gemm": {"B200CONV_GM": "2"},
+    "gemm-nosplit": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "1"},
+    "gemm-split3": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3"},
+    "gemm-dsmem": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "5", "B200CONV_TC_DSMEM": "1"},
+}
+
+
+@pytest.mark.parametrize("path", sorted(TC_PATHS))
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("i", [0, 1, 2, 5])
+def test_tc_paths_layers(conv, multi_oracle, monkeypatch, path, prec, i):
+    for k, v in TC_PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    I, F, Oo, A = multi_oracle(i)
+    assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"{MULTI[i]['name']} {prec} {path}")
+
+
+@pytest.mark.parametrize("path", sorted(TC_PATHS))
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_tc_paths_edges_and_ints(conv, monkeypatch, path, prec):
+    for k, v in TC_PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    for (C, Wx, Wy, K, M) in MULTI_EDGE:
+        I = synth.uniform01(31, (C, Wy, Wx))
+        F = synth.uniform_pm1(32, (M, C, K, K))
+        Oo, A = oracle.conv_multi(I, F)
+        assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"edge {C},{Wx},{Wy},{K},{M} {prec} {path}")
+    for (C, W, K, M) in [(64, 14, 3, 96), (96, 27, 5, 40), (512, 7, 3, 64), (16, 40, 3, 300)]:
+        I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
+        Oo, _ = oracle.conv_multi(I, F)
+        assert np.array_equal(run_multi(conv, I, F, prec), Oo), (C, W, K, M, prec, path)
