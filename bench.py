@@ -82,9 +82,19 @@ def suite(world: int = 1, rank: int = 0, precisions=("fp32", "tf32", "bf16")):
         c["bytes_alg"] = e * (c["C"] * c["Wx"] * c["Wy"] + c["M"] * c["C"] * c["K"] ** 2) \
             + 4 * c["M"] * c["Ho"] * c["Wo"]
         c["kernel"] = {"single": "KS"}.get(c["kind"]) or ("KM-SIMT" if c["prec"] == "fp32" else
-                                                         f"KM-TC-{c['prec']}")
+                                                         f"{_tc_name(c)}-{c['prec']}")
         c["label"] = f"{c['name']}:{c['prec']}"
     return calls
+
+
+def _tc_name(c):
+    """KM-TC (implicit kernel) or KM-TC/G (im2col + TMA GEMM pair), as planned."""
+    try:
+        from paper_2212_00404_b200 import conv
+        p = conv.plan_multi(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], c["prec"])
+        return "KM-TC/G" if p["kernel"] == 3 else "KM-TC"
+    except Exception:
+        return "KM-TC"
 
 
 def roof_for(c, pk):

@@ -30,12 +30,26 @@ for x in rows[hdr + 1:]:
         d[x[mi]] = v * scale
 calls = bench.suite()
 pk = bench.peaks()
+from paper_2212_00404_b200 import conv
+# one call of the hot path is plan["launches"] kernels (KM-SIMT workspace split:
+# main + reduce; KM-TC/G: im2col + GEMM): fold them into one row per call
+launches = sorted(per.items())
+merged, pos = [], 0
+for c in calls:
+    pl = (conv.plan_single(c["Wx"], c["Wy"], c["K"], c["M"]) if c["kind"] == "single"
+          else conv.plan_multi(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], c["prec"]))
+    parts = [d for _, d in launches[pos:pos + pl["launches"]]]
+    pos += pl["launches"]
+    m = {"kernel": " + ".join(d["kernel"].split("(")[0][:40] for d in parts)}
+    for key in ("us", "dram__bytes_read.sum", "dram__bytes_write.sum"):
+        m[key] = sum(d.get(key, 0) for d in parts)
+    merged.append((len(merged), m))
 out_rows, groups = [], {}
-for (i, d), c in zip(sorted(per.items()), calls):
+for (i, d), c in zip(merged, calls):
     b = bench.roof_for(c, pk)[0]
     key = f"{c['kernel']}/{b}"
     traffic = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-    out_rows.append([c["label"], key, d["kernel"][:60], round(d.get("us", 0), 3), int(traffic),
+    out_rows.append([c["label"], key, d["kernel"][:90], round(d.get("us", 0), 3), int(traffic),
                      int(c["bytes_alg"])])
     g = groups.setdefault(key, {"us": 0.0, "traffic": 0.0, "alg": 0.0, "n": 0})
     g["us"] += d.get("us", 0); g["traffic"] += traffic; g["alg"] += c["bytes_alg"]; g["n"] += 1
