@@ -272,6 +272,7 @@ int conv_version(void) { return (1 << 16) | 1; }
 // Max co-resident clusters for a kernel family at a cluster size (tools only).
 extern "C" B200CONV_API int conv_diag_stamps(unsigned long long *host) { return tc_read_stamps(host); }
 extern "C" B200CONV_API int conv_diag_ks_stamps(unsigned long long *host) { return ks_read_stamps(host); }
+extern "C" B200CONV_API int conv_diag_ks_fine(unsigned long long *host) { return ks_read_fine(host); }
 extern "C" B200CONV_API int conv_diag_tc_cta_stamps(unsigned long long *host) { return tc_read_cta_stamps(host); }
 extern "C" B200CONV_API int conv_diag_max_clusters(int kernel, int cluster, int smem_bytes) {
     return kernel == 2 ? tc_max_clusters(cluster, smem_bytes) : simt_max_clusters(cluster, smem_bytes);

@@ -58,10 +58,14 @@ struct KsArgs {
 // diagnostics (B200CONV_KS_DBG=1): per CTA [start, after griddepcontrol.wait,
 // staged, done << 8 | smid] globaltimer stamps of the last launch, CTAs 0..1023
 __device__ unsigned long long g_ks_stamps[4 * 1024];
+__device__ unsigned long long g_ks_fine[16];   // dbg == 2: CTA 0 warp 0 lane 0, first unit
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+int ks_read_fine(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_ks_fine, sizeof(g_ks_fine)) == cudaSuccess ? 0 : 1;
 }
 int ks_read_stamps(unsigned long long *host) {
     return cudaMemcpyFromSymbol(host, g_ks_stamps, sizeof(g_ks_stamps)) == cudaSuccess ? 0 : 1;
@@ -175,6 +179,8 @@ ks_kernel(const KsArgs a) {
     float w[R * KK];
     bool need_w = true;
     for (int u = w0; u < w1; ++u) {
+        const bool fine = a.dbg == 2 && blockIdx.x == 0 && threadIdx.x == 0 && u == w0;
+        if (fine) g_ks_fine[0] = gtimer();
         if (need_w) {                                 // (warp-uniform) new task: load its taps
             need_w = false;
             const float *ws = s_w + gi * GS;
@@ -186,6 +192,7 @@ ks_kernel(const KsArgs a) {
 #pragma unroll
             for (int q = (R * KK) & ~3; q < R * KK; ++q) w[q] = ws[q];
         }
+        if (fine) g_ks_fine[1] = gtimer();
         const int y0 = rb * RB + rg * RR;
         const int x = TX * xv;
         if (rg < a.RWt && y0 < Ho) {
@@ -218,6 +225,7 @@ ks_kernel(const KsArgs a) {
                         }
                     }
             }
+            if (fine) g_ks_fine[2] = gtimer() + (unsigned long long)(acc[0][0][0] == 12345.f);
             float *of = a.O + ((int64_t)g * R * Ho + y0) * Wo + x;
             const int nvs = min(TX, Wo - x);          // valid pixels of this slot (multiple of VS)
             const int nq = min(RR, Ho - y0), nf = min(R, M - g * R);
@@ -234,6 +242,7 @@ ks_kernel(const KsArgs a) {
                 }
             }
         }
+        if (fine) g_ks_fine[3] = gtimer();
         // next unit: next segment of this task, or segment 0 of the next task
         if (++j == nseg) {
             j = 0;
@@ -303,7 +312,7 @@ __host__ __device__ constexpr int ks_RR(int K) { return K <= 1 ? 1 : (K <= 3 ? 2
 
 struct KsPlan {
     KsArgs a;
-    int VL, VS, G, smem;
+    int RR, VL, VS, G, smem;
 };
 
 bool al(const void *p, int bytes) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % bytes == 0; }
@@ -331,7 +340,15 @@ void ks_cta_needs(const KsArgs &a, int K, int R, int RR, int TX, int G, int *gma
 bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O, KsPlan *kp) {
     if (K > 7) return false;
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
-    const int TX = ks_TX(K), R = ks_R(K), RR = ks_RR(K);
+    // small maps with K >= 3: one row per lane (a multi-row register block
+    // would be mostly rows past Ho, lengthening every warp's serial FMA chain)
+    // (measured, tools/ks_variants.py: 7x7 K=7 2.9 -> 2.2 us, 7x7 K=3 2.5 ->
+    // 2.0 us, 28x28 K=3 2.24 -> 2.05 us; K >= 5 at 28x28 and K = 3 at 56x56
+    // get slower).  B200CONV_KS_SMALL=<max Ho> overrides (0: off).
+    const char *sm = getenv("B200CONV_KS_SMALL");
+    const int small_ho = sm ? atoi(sm) : (K == 3 ? 32 : 16);
+    const bool small = K >= 3 && Ho <= small_ho;
+    const int TX = ks_TX(K), R = ks_R(K), RR = small ? 1 : ks_RR(K);
     KsArgs a = {};
     a.I = I; a.F = F; a.O = O;
     a.Wx = Wx; a.Wy = Wy; a.M = M;
@@ -365,7 +382,13 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
     // fairer across SMs; see tools/ks_variants.py)
     const int cap = (K == 1 ? 1 : ks_min_blocks(K)) * kNumSMs;
     const int max_smem = (ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
+    // (B200CONV_KS_SPREAD=1: at least one CTA per SM up to one unit per CTA;
+    // measured neutral on the small maps, so off by default)
     int G = (a.U + kKsWarps - 1) / kKsWarps;
+    if (const char *e = getenv("B200CONV_KS_SPREAD"); e && e[0] == '1') {
+        const int spread = a.U < kNumSMs ? a.U : kNumSMs;
+        if (G < spread) G = spread;
+    }
     if (G > cap) G = cap;
     if (const char *e = getenv("B200CONV_KS_G")) {        // experiments: CTA count override
         const int g = atoi(e);
@@ -380,8 +403,10 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
         if (smem <= max_smem || G >= a.U) {
             if (smem > 200 * 1024) return false;
             kp->a = a;
+            kp->RR = RR;
             kp->VL = (Wx % TX == 0 && al(I, 4 * TX)) ? TX : 1;
             kp->VS = (Wo % TX == 0 && al(O, 4 * TX)) ? TX : ((TX >= 2 && Wo % 2 == 0 && al(O, 8)) ? 2 : 1);
+            if (RR != ks_RR(K)) kp->VL = kp->VS = 1;    // small-map variant: scalar loads / stores
             kp->G = G;
             kp->smem = smem;
             return true;
@@ -407,7 +432,7 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
         p->grid_y = 1;
         p->grid_z = 1;
         p->tile_m = ks_R(K);                              // filters per task
-        p->tile_n = kp.a.RWt * ks_RR(K);                  // output rows per task (full width)
+        p->tile_n = kp.a.RWt * kp.RR;                     // output rows per task (full width)
         p->smem_bytes = kp.smem;
         return 0;
     }
@@ -430,9 +455,9 @@ static cudaLaunchAttribute pdl_attr() {
     return a;
 }
 
-template <int K, int VL, int VS>
+template <int K, int VL, int VS, int RR = ks_RR(K)>
 static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
-    auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R(K), ks_RR(K)>;
+    auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R(K), RR>;
     if (kp.smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.smem);
         if (e != cudaSuccess) return e;
@@ -456,6 +481,8 @@ template <int K>
 static cudaError_t launch_ks_v(const KsPlan &kp, cudaStream_t s) {
     constexpr int TX = ks_TX(K);
     constexpr int V2 = TX >= 2 ? 2 : 1;
+    if constexpr (ks_RR(K) != 1)
+        if (kp.RR == 1) return launch_ks<K, 1, 1, 1>(kp, s);
     if (kp.VL == TX) {
         if (kp.VS == TX) return launch_ks<K, TX, TX>(kp, s);
         if (kp.VS == 2) return launch_ks<K, TX, V2>(kp, s);

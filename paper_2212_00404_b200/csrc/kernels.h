@@ -57,6 +57,7 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
 int tc_max_clusters(int cluster, int smem);
 int tc_read_stamps(unsigned long long *host);
 int ks_read_stamps(unsigned long long *host);
+int ks_read_fine(unsigned long long *host);
 int tc_read_cta_stamps(unsigned long long *host);
 int simt_max_clusters(int cluster, int smem);
 

@@ -47,3 +47,10 @@ for i in range(0, len(args), 3):
     print("  earliest SMs:", [(k, per_sm[k]) for k in ks[-4:]])
     cnt = np.bincount([len(v) for v in per_sm.values()])
     print("  CTAs per SM histogram:", cnt.tolist(), "SMs used", len(per_sm))
+    os.environ["B200CONV_KS_DBG"] = "2"
+    for O in Os: conv.conv_single_ex(I, W, W, F, K, M, O)
+    torch.cuda.synchronize()
+    fb = (ctypes.c_ulonglong * 16)()
+    lib.conv_diag_ks_fine(fb)
+    f = np.array(list(fb)[:4], dtype=np.int64)
+    print("  CTA0 warp0 unit0: taps %.3f us, compute %.3f us, stores %.3f us" % ((f[1] - f[0]) / 1e3, (f[2] - f[1]) / 1e3, (f[3] - f[2]) / 1e3))

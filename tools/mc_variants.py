@@ -1,6 +1,6 @@
 """Back-to-back (CUDA graph, 12 launches, rotating O) time of multi-channel
 bench layers under environment variants.
-usage: mc_variants.py "ENV=v,ENV2=w;..." <label-substring> [...]"""
+usage: mc_variants.py "ENV=v&ENV2=w;..." <label-substring> [...]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -40,7 +40,7 @@ for want in sys.argv[2:]:
         Os = [torch.empty((c["M"], c["Ho"], c["Wo"]), device=dev) for _ in range(nb)]
         out = []
         for v in variants:
-            env = dict(kv.split("=") for kv in v.split(",") if kv)
+            env = dict(kv.split("=", 1) for kv in v.split("&") if kv)
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             us = timeit(lambda j: conv.conv_multi_ex(I, c["C"], c["Wx"], c["Wy"], Fs[j % nb], c["K"], c["M"],
@@ -50,4 +50,3 @@ for want in sys.argv[2:]:
                 else: os.environ[k] = o
             out.append(f"{v or 'base'}: {us:6.2f}")
         print(f"{c['label']}: " + " | ".join(out), flush=True)
-        break
