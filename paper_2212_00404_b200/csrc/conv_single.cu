@@ -53,6 +53,7 @@ struct KsArgs {
     int ub, ur;   // U = ub * NW + ur: warp w owns units [w*ub + min(w, ur), (w+1)*ub + min(w+1, ur))
     int gmax;     // filter-group capacity of the smem tap table
     int dbg;      // diagnostics: 1 = per-CTA globaltimer stamps into g_ks_stamps
+    int prefetch; // L2 prefetch of the CTA's inputs before griddepcontrol.wait (B200CONV_PREFETCH=0: off)
 };
 
 // diagnostics (B200CONV_KS_DBG=1): per CTA [start, after griddepcontrol.wait,
@@ -139,6 +140,15 @@ ks_kernel(const KsArgs a) {
     const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
     const int pad = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3);
 
+    // warm L2 with this CTA's input rows and taps while the previous kernel drains
+    if (a.prefetch) {
+    for (int64_t e = e0 + 32 * tid; e < e1; e += 32 * kKsThreads) prefetch_l2(a.I + e);
+    if (tid < ngr) {
+        int g = g_first + tid;
+        if (g >= NG) g -= NG;
+        prefetch_l2(a.F + (int64_t)g * R * KK);
+    }
+    }
     pdl_wait();
     if (stamp) g_ks_stamps[4 * blockIdx.x + 1] = gtimer();
     for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
@@ -473,6 +483,8 @@ static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
     KsArgs a = kp.a;
     const char *dbg = getenv("B200CONV_KS_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
+    const char *pf = getenv("B200CONV_PREFETCH");
+    a.prefetch = !(pf && pf[0] == '0');
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -228,6 +228,12 @@ __device__ __forceinline__ void bulk_wait() {           // all but N newest grou
 // Programmatic dependent launch: let the next kernel in the stream start its
 // prologue early; wait for the previous grid (and its memory) before touching
 // global memory, so dependent chains of calls stay correct.
+// L2 prefetch of a line.  Issued BEFORE griddepcontrol.wait it only warms L2
+// (the coherence point) — the data are read after the wait — so it is safe
+// even if the previous kernel writes the same lines.
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
