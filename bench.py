@@ -462,6 +462,39 @@ def _strong_sweep(args, conv, dev, stream, world, rank, cacheI):
         flop = 2.0 * c["M"] * c["C"] * c["K"] ** 2 * Ho * Wo
         out[prec] = {"us_max_rank": round(us, 3), "gflops_total": round(flop / (us * 1e-6) / 1e9, 1),
                      "filters_per_rank": Mloc}
+        if world > 1:
+            # G2 of SURVEY §8(a): the path's only collective, the all-gather of
+            # the filter-sharded O (NCCL over NVLink), timed with and without
+            # the convolution (device events, max over ranks)
+            try:
+                from paper_2212_00404_b200.shard import allgather_output
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        allgather_output(O, c["M"])
+                    dist.barrier()
+                    stream.synchronize()
+                    e0.record(stream)
+                    for _ in range(reps):
+                        allgather_output(O, c["M"])
+                    e1.record(stream)
+                    stream.synchronize()
+                    ag = 1e3 * e0.elapsed_time(e1) / reps
+                    dist.barrier()
+                    stream.synchronize()
+                    e0.record(stream)
+                    for _ in range(reps):
+                        conv.conv_multi_ex(I, c["C"], c["Wx"], c["Wy"], F, c["K"], Mloc, O, prec, stream.cuda_stream)
+                        allgather_output(O, c["M"])
+                    e1.record(stream)
+                    stream.synchronize()
+                    both = 1e3 * e0.elapsed_time(e1) / reps
+                tt = torch.tensor([ag, both], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                out[prec]["allgather_us_max_rank"] = round(float(tt[0]), 3)
+                out[prec]["conv_plus_allgather_us_max_rank"] = round(float(tt[1]), 3)
+                out[prec]["allgather_bytes_per_rank_recv"] = int(4 * (c["M"] - Mloc) * Ho * Wo)
+            except Exception as exc:  # reported, never fatal for the bench line
+                out[prec]["allgather_error"] = repr(exc)[:200]
     return out
 
 

@@ -498,6 +498,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                 for (int t = 0; t < S; ++t) bulk_load(slices + t * rows * kTcBM, wt + t * wslice, bytes, red_bar);
             }
             mbar_wait(red_bar, 0);
+            if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 7] = tc_gtimer();
         }
         for (int idx = threadIdx.x; idx < rows * (kTcBM / 4); idx += kTcThreads) {
             const int nl = nlo + idx / (kTcBM / 4), row0 = 4 * (idx % (kTcBM / 4));

@@ -32,8 +32,9 @@ for want in sys.argv[1:]:
         tu[:, 5] |= tu[:, 0] & ~np.uint64((1 << 56) - 1)
         t = tu.astype(np.int64)
         t[:, 6] = np.where(t[:, 6] == 0, t[:, 4], t[:, 6])
+        t[:, 7] = np.where(t[:, 7] == 0, t[:, 6], t[:, 7])
         r = (t - t[:, 0].min()) / 1e3
         print(f"== {c['label']} plan {p} CTAs {G} (pctl 0/50/90/100, us)")
-        for k, name in [(0, "start"), (1, "pdl-wait"), (2, "kb0 ready"), (3, "mma done"), (4, "epilogue"), (6, "clustersync"), (5, "end")]:
+        for k, name in [(0, "start"), (1, "pdl-wait"), (2, "kb0 ready"), (3, "mma done"), (4, "epilogue"), (6, "clustersync"), (7, "slices in"), (5, "end")]:
             print(f"  {name:10s}", " ".join(f"{v:6.2f}" for v in np.percentile(r[:, k], [0, 50, 90, 100])))
         break
