@@ -527,8 +527,9 @@ def _cudnn_context(args, calls, dev, stream, capture, pk):
 
 
 def _e2e(args, conv, calls, stream, world, rank, dev):
-    """Same metric through the public host-buffer API (conv_*_host): per layer,
-    H2D of I and F from pinned memory, the kernel, D2H of O, stream sync."""
+    """Same metric through the public host-buffer API (conv_*_host_async): per
+    layer, H2D of I and F from pinned memory, the kernel(s), D2H of O; calls
+    alternate between two streams; the host waits once per step."""
     import torch
     import torch.distributed as dist
     steps = max(1, min(args.steps, args.e2e_steps))
@@ -540,16 +541,27 @@ def _e2e(args, conv, calls, stream, world, rank, dev):
         host.append((Ih, Fh, Oh))
     h2d = sum(Ih.numel() * Ih.element_size() + Fh.numel() * Fh.element_size() for Ih, Fh, _ in host)
     d2h = sum(Oh.numel() * 4 for _, _, Oh in host)
-    sh = stream.cuda_stream
+    # the asynchronous host entry points on --e2e-streams streams (round robin
+    # per call): one call's device->host copy overlaps the next calls'
+    # host->device copies and kernels (several streams, so a copy queued behind
+    # its stream's previous device->host copy does not block the copy engine's
+    # queue for the others); one host synchronisation per step
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(args.e2e_streams - 1)]
+    done = [torch.cuda.Event() for _ in streams]
 
     def one_step():
-        for c, (Ih, Fh, Oh) in zip(calls, host):
+        for i, (c, (Ih, Fh, Oh)) in enumerate(zip(calls, host)):
+            sh = streams[i % len(streams)].cuda_stream
             if c["kind"] == "single":
-                conv.conv_single_host(Ih, c["Wx"], c["Wy"], Fh, c["K"], c["M"], Oh, sh)
+                conv.conv_single_host_async(Ih, c["Wx"], c["Wy"], Fh, c["K"], c["M"], Oh, sh)
             else:
-                conv.conv_multi_host(Ih, c["C"], c["Wx"], c["Wy"], Fh, c["K"], c["M"], Oh, c["prec"], sh)
+                conv.conv_multi_host_async(Ih, c["C"], c["Wx"], c["Wy"], Fh, c["K"], c["M"], Oh, c["prec"], sh)
+        for st, ev in zip(streams[1:], done[1:]):
+            ev.record(st)
+            stream.wait_event(ev)
 
-    one_step()                                   # warm-up
+    one_step()                                   # warm-up (pool, workspaces)
+    stream.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -557,6 +569,7 @@ def _e2e(args, conv, calls, stream, world, rank, dev):
     e0.record(stream)
     for _ in range(steps):
         one_step()
+        stream.synchronize()                     # results on the host once per step
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -567,7 +580,8 @@ def _e2e(args, conv, calls, stream, world, rank, dev):
     flop = world * sum(c["flop"] for c in calls)
     return {"value": round(flop / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "ms_per_step": round(ms, 3),
             "steps": steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "conv_single_host / conv_multi_host (pinned host buffers, one sync per layer)"}
+            "api": f"conv_single_host_async / conv_multi_host_async (pinned host buffers, "
+                   f"{len(streams)} streams round robin per call, one host synchronisation per step)"}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -647,6 +661,7 @@ def main():
     ap.add_argument("--cudnn", type=int, default=1)
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-streams", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     args = ap.parse_args()

@@ -104,13 +104,26 @@ B200CONV_API int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void 
 
 /* End-to-end entry points on HOST buffers (pageable or pinned): copy I and F
  * host->device, run the same kernels as the *_ex calls, copy O device->host,
- * and synchronise the stream before returning.  Device scratch is allocated
- * and freed stream-ordered (cudaMallocAsync) inside the call.  For CONV_BF16
+ * and synchronise the stream before returning.  Device scratch comes from a
+ * library-owned stream-ordered memory pool (allocated once, then reused).  For CONV_BF16
  * the host I and F are bfloat16 arrays. */
 B200CONV_API int conv_single_host(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                      void *stream);
 B200CONV_API int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                     int precision, void *stream);
+
+/* Asynchronous host-buffer entry points: the same copies and kernels enqueued
+ * on `stream`, WITHOUT the final synchronisation, so a caller can keep several
+ * calls in flight on different streams and overlap their host->device and
+ * device->host copies (two copy engines).  I, F and O must be page-locked
+ * (cudaHostAlloc / torch pin_memory) for the copies to be asynchronous; they
+ * must stay valid, and O must not be read, until the caller synchronises
+ * `stream`.  Argument errors are returned before anything is enqueued; copy
+ * or kernel faults surface at that synchronisation. */
+B200CONV_API int conv_single_host_async(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                           void *stream);
+B200CONV_API int conv_multi_host_async(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                          int precision, void *stream);
 
 /* Launch plan the device entry points use for a shape (pure function; no
  * device access).  A call of the hot path is one kernel launch, or two when

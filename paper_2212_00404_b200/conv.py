@@ -27,7 +27,7 @@ PRECISIONS = {"fp32": CONV_FP32, "tf32": CONV_TF32, "bf16": CONV_BF16}
 STATUS = {0: "CONV_OK", 1: "CONV_E_SHAPE", 2: "CONV_E_NULL", 3: "CONV_E_ALIGN",
           4: "CONV_E_PRECISION", 5: "CONV_E_DEVICE", 6: "CONV_E_LAUNCH"}
 EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv_single_host",
-           "conv_multi_host", "conv_plan_single", "conv_plan_multi", "conv_status_string",
+           "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_plan_single", "conv_plan_multi", "conv_status_string",
            "conv_version"]
 
 
@@ -66,6 +66,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.conv_multi_ex.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
             lib.conv_single_host.argtypes = [P, I32, I32, P, I32, I32, P, P]
             lib.conv_multi_host.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
+            lib.conv_single_host_async.argtypes = [P, I32, I32, P, I32, I32, P, P]
+            lib.conv_multi_host_async.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
             lib.conv_plan_single.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
             lib.conv_plan_multi.argtypes = [I32, I32, I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
             lib.conv_status_string.argtypes = [I32]
@@ -123,6 +125,17 @@ def conv_multi_ex(I, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):
 
 def conv_single_host(I, Wx, Wy, F, K, M, O, stream=None):
     _check(load().conv_single_host(_ptr(I), Wx, Wy, _ptr(F), K, M, _ptr(O), _stream(stream)))
+
+
+def conv_single_host_async(I, Wx, Wy, F, K, M, O, stream=None):
+    """As conv_single_host without the final stream synchronisation (pinned buffers)."""
+    _check(load().conv_single_host_async(_ptr(I), Wx, Wy, _ptr(F), K, M, _ptr(O), _stream(stream)))
+
+
+def conv_multi_host_async(I, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):
+    """As conv_multi_host without the final stream synchronisation (pinned buffers)."""
+    _check(load().conv_multi_host_async(_ptr(I), C, Wx, Wy, _ptr(F), K, M, _ptr(O), _prec(precision),
+                                        _stream(stream)))
 
 
 def conv_multi_host(I, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):

@@ -151,6 +151,13 @@ static cudaMemPool_t host_pool() {
         if (cudaMemPoolCreate(&p, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
         uint64_t keep = UINT64_MAX;
         cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        // a block freed on one stream is reused only by that stream: cross-
+        // stream reuse would insert a wait on the freeing stream and serialise
+        // callers that overlap copies on several streams (*_host_async)
+        int no = 0;
+        cudaMemPoolSetAttribute(p, cudaMemPoolReuseFollowEventDependencies, &no);
+        cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &no);
+        cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &no);
         pools[dev] = p;
     }
     return pools[dev];
@@ -163,7 +170,8 @@ static cudaError_t pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
 
 static int host_roundtrip(const void *Ih, size_t i_bytes, const void *Fh, size_t f_bytes, float *Oh,
                           size_t o_bytes, cudaStream_t s,
-                          int (*body)(const void *, const void *, float *, void *), void *ctx) {
+                          int (*body)(const void *, const void *, float *, void *), void *ctx,
+                          bool sync = true) {
     void *Id = nullptr, *Fd = nullptr, *Od = nullptr;
     if (pool_alloc(&Id, i_bytes, s) != cudaSuccess || pool_alloc(&Fd, f_bytes, s) != cudaSuccess ||
         pool_alloc(&Od, o_bytes, s) != cudaSuccess) {
@@ -182,7 +190,7 @@ static int host_roundtrip(const void *Ih, size_t i_bytes, const void *Fh, size_t
     cudaFreeAsync(Id, s);
     cudaFreeAsync(Fd, s);
     cudaFreeAsync(Od, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess && st == CONV_OK) st = CONV_E_LAUNCH;
+    if (sync && cudaStreamSynchronize(s) != cudaSuccess && st == CONV_OK) st = CONV_E_LAUNCH;
     cudaGetLastError();
     return st;
 }
@@ -222,6 +230,33 @@ int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, 
     const size_t Ho = Wy - K + 1, Wo = Wx - K + 1;
     return host_roundtrip(I, (size_t)C * Wx * Wy * e, F, (size_t)M * C * K * K * e, O,
                           (size_t)M * Ho * Wo * 4, ctx.s, multi_body, &ctx);
+}
+
+// Asynchronous variants: identical, minus the final stream synchronisation.
+int conv_single_host_async(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
+                           void *stream) {
+    int st = check_shape(1, Wx, Wy, K, M);
+    if (st) return st;
+    if ((st = check_ptrs(I, F, O, 4))) return st;
+    if ((st = check_device())) return st;
+    MultiCtx ctx{1, Wx, Wy, K, M, CONV_FP32, static_cast<cudaStream_t>(stream)};
+    const size_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    return host_roundtrip(I, (size_t)Wx * Wy * 4, F, (size_t)M * K * K * 4, O, (size_t)M * Ho * Wo * 4,
+                          ctx.s, single_body, &ctx, false);
+}
+
+int conv_multi_host_async(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                          int precision, void *stream) {
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    const int e = precision == CONV_BF16 ? 2 : 4;
+    if ((st = check_ptrs(I, F, O, e))) return st;
+    if ((st = check_device())) return st;
+    MultiCtx ctx{C, Wx, Wy, K, M, precision, static_cast<cudaStream_t>(stream)};
+    const size_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    return host_roundtrip(I, (size_t)C * Wx * Wy * e, F, (size_t)M * C * K * K * e, O,
+                          (size_t)M * Ho * Wo * 4, ctx.s, multi_body, &ctx, false);
 }
 
 // ------------------------------------------------------------ plans / misc
@@ -264,7 +299,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 1; }
+int conv_version(void) { return (1 << 16) | 2; }   // 1.2: + *_host_async
 
 }  // extern "C"
 

@@ -22,11 +22,11 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 10
+    assert len(syms) == 12
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16) | 1
+    assert conv.version() == (1 << 16) | 2
 
 
 def test_status_strings():

@@ -227,6 +227,31 @@ def test_host_entry_points(conv):
     assert_parity(Og, Oo, A, TAU["fp32"], "host single")
 
 
+def test_host_async_entry_points_two_streams(conv):
+    # several calls in flight on two streams, pinned host buffers, one sync at the end
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    cases = []
+    for i, (C, W, K, M, prec) in enumerate([(64, 14, 3, 96, "fp32"), (1, 56, 3, 64, "single"),
+                                             (32, 28, 3, 128, "bf16"), (512, 7, 3, 512, "tf32"),
+                                             (3, 40, 5, 70, "tf32"), (1, 224, 1, 32, "single")]):
+        I, F = synth.layer_inputs(C, W, W, K, M, cfg_index=40 + i)
+        Oo, A = oracle.conv_multi(I, F)
+        dt = torch.bfloat16 if prec == "bf16" else torch.float32
+        Ih = torch.from_numpy(I[0] if prec == "single" else I).to(dt).pin_memory()
+        Fh = torch.from_numpy(F[:, 0] if prec == "single" else F).to(dt).pin_memory()
+        Oh = torch.full((M, W - K + 1, W - K + 1), float("nan")).pin_memory()
+        sh = streams[i & 1].cuda_stream
+        if prec == "single":
+            conv.conv_single_host_async(Ih, W, W, Fh, K, M, Oh, sh)
+        else:
+            conv.conv_multi_host_async(Ih, C, W, W, Fh, K, M, Oh, prec, sh)
+        cases.append((Oh, Oo, A, "fp32" if prec == "single" else prec))
+    for st in streams:
+        st.synchronize()
+    for Oh, Oo, A, prec in cases:
+        assert_parity(Oh.numpy().astype(np.float64), Oo, A, TAU[prec], f"host async {prec}")
+
+
 def test_output_untouched_on_argument_error(conv):
     O = torch.full((4, 6, 6), 7.0, device="cuda")
     I = torch.rand(8, 8, device="cuda")
