@@ -64,6 +64,12 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *m, uin
           "r"(c0), "r"(c1) : "memory");
 }
 
+// L2 prefetch of a TMA tile (no smem destination, no completion); safe before
+// griddepcontrol.wait for the same reason as prefetch_l2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+                 ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void *dst, const CUtensorMap *m, uint64_t *bar,
                                             int32_t c0) {
     asm volatile(

@@ -4,6 +4,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 from paper_2212_00404_b200 import conv
+if os.environ.get("B200CONV_LIB_PATH"):           # A/B against another build of the library
+    conv.load(os.environ["B200CONV_LIB_PATH"])
 dev = torch.device("cuda", 0)
 s = torch.cuda.Stream()
 variants = [v for v in sys.argv[1].split(";")]

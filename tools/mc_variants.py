@@ -6,6 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench, synth
 from paper_2212_00404_b200 import conv
+if os.environ.get("B200CONV_LIB_PATH"):           # A/B against another build of the library
+    conv.load(os.environ["B200CONV_LIB_PATH"])
 dev = torch.device("cuda", 0)
 s = torch.cuda.Stream()
 variants = sys.argv[1].split(";")
