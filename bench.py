@@ -529,7 +529,8 @@ def _cudnn_context(args, calls, dev, stream, capture, pk):
 def _e2e(args, conv, calls, stream, world, rank, dev):
     """Same metric through the public host-buffer API (conv_*_host_async): per
     layer, H2D of I and F from pinned memory, the kernel(s), D2H of O; calls
-    alternate between two streams; the host waits once per step."""
+    round-robin over --e2e-streams streams in an order that interleaves
+    output-heavy and input-heavy layers; the host waits once per step."""
     import torch
     import torch.distributed as dist
     steps = max(1, min(args.steps, args.e2e_steps))
@@ -548,9 +549,24 @@ def _e2e(args, conv, calls, stream, world, rank, dev):
     # queue for the others); one host synchronisation per step
     streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(args.e2e_streams - 1)]
     done = [torch.cuda.Event() for _ in streams]
+    # issue order: the layers of a step are independent problems, so the caller
+    # interleaves output-heavy calls (224x224 maps) with input-heavy ones (big
+    # filter banks) to keep both PCIe directions busy at once
+    net = [Oh.numel() * 4 - Ih.numel() * Ih.element_size() - Fh.numel() * Fh.element_size()
+           for Ih, Fh, Oh in host]
+    by = sorted(range(len(calls)), key=lambda i: net[i])
+    order = []
+    lo, hi = 0, len(by) - 1
+    while lo <= hi:
+        order.append(by[hi]); hi -= 1
+        if lo <= hi:
+            order.append(by[lo]); lo += 1
+    if not args.e2e_interleave:
+        order = list(range(len(calls)))
 
     def one_step():
-        for i, (c, (Ih, Fh, Oh)) in enumerate(zip(calls, host)):
+        for i, j in enumerate(order):
+            c, (Ih, Fh, Oh) = calls[j], host[j]
             sh = streams[i % len(streams)].cuda_stream
             if c["kind"] == "single":
                 conv.conv_single_host_async(Ih, c["Wx"], c["Wy"], Fh, c["K"], c["M"], Oh, sh)
@@ -581,7 +597,9 @@ def _e2e(args, conv, calls, stream, world, rank, dev):
     return {"value": round(flop / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "ms_per_step": round(ms, 3),
             "steps": steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": f"conv_single_host_async / conv_multi_host_async (pinned host buffers, "
-                   f"{len(streams)} streams round robin per call, one host synchronisation per step)"}
+                   f"{len(streams)} streams round robin per call, "
+                   f"{'output-/input-heavy calls interleaved' if args.e2e_interleave else 'suite order'}, "
+                   f"one host synchronisation per step)"}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -662,6 +680,7 @@ def main():
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-streams", type=int, default=8)
+    ap.add_argument("--e2e-interleave", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     args = ap.parse_args()
