@@ -37,6 +37,23 @@ constexpr int kSimtThreads = 256;              // (BM/8) x (BN/8) threads, 8x8 o
 constexpr int kSimtMaxSplit = 16;              // non-portable cluster size on B200
 constexpr int kSimtMaxSmem = 110 * 1024;       // 2 CTAs per SM
 
+// diagnostics (B200CONV_SIMT_DBG=1): per-CTA globaltimer stamps [start, after
+// griddepcontrol.wait, chunk 0 staged, main loop done, end << 8 | smid]
+__device__ unsigned long long g_simt_cta[5 * 1024];
+__device__ __forceinline__ unsigned long long simt_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long simt_smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+int simt_read_stamps(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_simt_cta, sizeof(g_simt_cta)) == cudaSuccess ? 0 : 1;
+}
+
 // Fallback for shapes whose chunk does not fit in shared memory (huge K):
 // one thread per output, loads through L1.
 __global__ void __launch_bounds__(256)
@@ -84,8 +101,11 @@ struct SimtShape {
 template <int BM, int BN, int TN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
-           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W) {
+           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg) {
     using SH = SimtShape<BM, BN, TN>;
+    const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool tl = dbg && threadIdx.x == 0 && cta_lin < 1024;
+    if (tl) g_simt_cta[5 * cta_lin] = simt_gtimer();
     constexpr int NT = kSimtThreads;
     constexpr int TNG = SH::TNG;
     constexpr int T2 = SH::T2;
@@ -197,6 +217,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
 
     pdl_wait();
     pdl_trigger();
+    if (tl) g_simt_cta[5 * cta_lin + 1] = simt_gtimer();
     __syncthreads();                                // koff table
     if (nchunks > 0) {
         load_f(0);
@@ -204,6 +225,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
+        if (tl) g_simt_cta[5 * cta_lin + 2] = simt_gtimer();
         transpose_f();
         __syncthreads();
         if (nchunks > 1) { load_f(1); load_b(1, 1); }
@@ -244,6 +266,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         }
     }
     cp_async_wait<0>();
+    if (tl) g_simt_cta[5 * cta_lin + 3] = simt_gtimer();
 
     if (W != nullptr) {
         // ---- workspace split-K: partial tile -> W[split] (padded, aligned) ----
@@ -260,6 +283,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
             else if constexpr (T2 == 2)
                 __stcg(reinterpret_cast<float2 *>(wr + SH::R1 + tn * 2), make_float2(acc[i][4], acc[i][5]));
         }
+        if (tl) g_simt_cta[5 * cta_lin + 4] = simt_gtimer() << 8 | simt_smid();
         return;
     }
     __syncthreads();
@@ -300,6 +324,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         }
     }
     if (S > 1) cluster_sync_all();
+    if (tl) g_simt_cta[5 * cta_lin + 4] = simt_gtimer() << 8 | simt_smid();
 }
 
 namespace {
@@ -491,7 +516,9 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = W ? 1 : 2;
-    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W);
+    const char *dbgs = getenv("B200CONV_SIMT_DBG");
+    const int dbg = dbgs ? atoi(dbgs) : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg);
     if (e != cudaSuccess || !W) return e;
     const int ldw = p.grid_y * BN;
     const int64_t slice = (int64_t)p.grid_z * BM * ldw;

@@ -230,6 +230,13 @@ __device__ __forceinline__ void bulk_wait() {           // all but N newest grou
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------- gpu-scope flags
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: let the next kernel in the stream start its
 // prologue early; wait for the previous grid (and its memory) before touching
