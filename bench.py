@@ -195,10 +195,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (B200CONV_BENCH_BACKEND=gloo + more ranks than GPUs: a functional check of
+    # the N > 1 path on one GPU — ranks share devices; its timings mean nothing)
+    backend = os.environ.get("B200CONV_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     conv.load()
     pk = peaks()
     precisions = tuple(args.precision.split(","))
