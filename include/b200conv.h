@@ -102,6 +102,16 @@ B200CONV_API int conv_single_ex(const float *I, int Wx, int Wy, const float *F, 
 B200CONV_API int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                   int precision, void *stream);
 
+/* Batch of N images sharing one filter bank (the layers as CNNs run them,
+ * P:25-42): I [N][C][Wy][Wx], O [N][M][Wy-K+1][Wx-K+1] (device
+ * pointers, same element types as conv_multi_ex).  TF32 / BF16: ONE launch of
+ * the implicit tensor-core kernel whose pixel tiles span all N images (no
+ * split-K needed once N fills the machine).  CONV_FP32 (and N == 1): one
+ * conv_multi_ex launch per image.  N < 1 or N*C*Wx*Wy / N*M*Ho*Wo > INT_MAX:
+ * CONV_E_SHAPE; other errors as conv_multi_ex. */
+B200CONV_API int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M,
+                          float *O, int precision, void *stream);
+
 /* End-to-end entry points on HOST buffers (pageable or pinned): copy I and F
  * host->device, run the same kernels as the *_ex calls, copy O device->host,
  * and synchronise the stream before returning.  Device scratch comes from a
@@ -146,6 +156,8 @@ typedef struct {
 
 B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);
 B200CONV_API int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
+/* Plan of conv_multi_batched_ex (for CONV_FP32 / N == 1: the per-image plan). */
+B200CONV_API int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
 
 B200CONV_API const char *conv_status_string(int status);
 

@@ -27,7 +27,8 @@ PRECISIONS = {"fp32": CONV_FP32, "tf32": CONV_TF32, "bf16": CONV_BF16}
 STATUS = {0: "CONV_OK", 1: "CONV_E_SHAPE", 2: "CONV_E_NULL", 3: "CONV_E_ALIGN",
           4: "CONV_E_PRECISION", 5: "CONV_E_DEVICE", 6: "CONV_E_LAUNCH"}
 EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv_single_host",
-           "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_plan_single", "conv_plan_multi", "conv_status_string",
+           "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_multi_batched_ex",
+           "conv_plan_multi_batched", "conv_plan_single", "conv_plan_multi", "conv_status_string",
            "conv_version"]
 
 
@@ -70,6 +71,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.conv_multi_host_async.argtypes = [P, I32, I32, I32, P, I32, I32, P, I32, P]
             lib.conv_plan_single.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
             lib.conv_plan_multi.argtypes = [I32, I32, I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
+            lib.conv_multi_batched_ex.argtypes = [P, I32, I32, I32, I32, P, I32, I32, P, I32, P]
+            lib.conv_plan_multi_batched.argtypes = [I32, I32, I32, I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
             lib.conv_status_string.argtypes = [I32]
             lib.conv_status_string.restype = ctypes.c_char_p
             lib.conv_version.argtypes = []
@@ -149,6 +152,17 @@ def plan_single(Wx, Wy, K, M) -> dict:
     return p.as_dict()
 
 
+def conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision="fp32", stream=None):
+    _check(load().conv_multi_batched_ex(_ptr(I), N, C, Wx, Wy, _ptr(F), K, M, _ptr(O), _prec(precision),
+                                        _stream(stream)))
+
+
+def plan_multi_batched(N, C, Wx, Wy, K, M, precision="fp32") -> dict:
+    p = ConvPlan()
+    _check(load().conv_plan_multi_batched(N, C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
+    return p.as_dict()
+
+
 def plan_multi(C, Wx, Wy, K, M, precision="fp32") -> dict:
     p = ConvPlan()
     _check(load().conv_plan_multi(C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
@@ -194,6 +208,24 @@ def multi(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor 
     O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), device=I.device,
                                                 dtype=torch.float32)
     conv_multi_ex(I, C, Wx, Wy, F, K, M, O, precision, stream)
+    return O
+
+
+def multi_batched(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor | None = None,
+                  stream=None):
+    """Eq. 1 on a batch: I[N][C][Wy][Wx], F[M][C][K][K] -> O[N][M][Ho][Wo] f32
+    (= torch.nn.functional.conv2d(I, F) without padding, stride 1)."""
+    _require_cuda(I, F)
+    want = torch.bfloat16 if _prec(precision) == CONV_BF16 else torch.float32
+    if I.dtype != want or F.dtype != want:
+        raise ValueError(f"precision {precision} expects {want} inputs")
+    N, C, Wy, Wx = I.shape
+    M, C2, K, _ = F.shape
+    if C2 != C:
+        raise ValueError("channel mismatch")
+    O = out if out is not None else torch.empty((N, M, Wy - K + 1, Wx - K + 1), device=I.device,
+                                                dtype=torch.float32)
+    conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision, stream)
     return O
 
 

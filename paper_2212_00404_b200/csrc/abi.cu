@@ -30,7 +30,8 @@ int b200::choose_split(int tiles, int units, int max_split, int ctas_per_sm, flo
     float best_t = -1.f;
     for (int S = 1; S <= (max_split < 1 ? 1 : max_split); ++S) {
         const int waves = (tiles + tab[S] - 1) / tab[S];
-        const float t = waves * ((units + S - 1) / S) * t_unit + (S > 1 ? t_reduce : 0.f);
+        // every wave of clusters pays its own partial exchange
+        const float t = waves * (((units + S - 1) / S) * t_unit + (S > 1 ? t_reduce : 0.f));
         if (best_t < 0.f || t < best_t - 1e-6f) { best_t = t; best = S; }
     }
     return best;
@@ -130,6 +131,31 @@ int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, in
 
 int conv_multi(const float *I, int C, int Wx, int Wy, const float *F, int K, int M, float *O) {
     return conv_multi_ex(I, C, Wx, Wy, F, K, M, O, CONV_FP32, nullptr);
+}
+
+int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                          int precision, void *stream) {
+    if (N < 1) return CONV_E_SHAPE;
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    const int64_t Ho = Wy - K + 1, Wo = Wx - K + 1;
+    if ((int64_t)N * C * Wx * Wy > INT_MAX || (int64_t)N * M * Ho * Wo > INT_MAX) return CONV_E_SHAPE;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    const int e = precision == CONV_BF16 ? 2 : 4;
+    if ((st = check_ptrs(I, F, O, e))) return st;
+    if ((st = check_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (precision == CONV_FP32 || N == 1) {
+        // strict FP32 (and N == 1): one call per image
+        for (int n = 0; n < N; ++n) {
+            st = run_multi(static_cast<const uint8_t *>(I) + (size_t)n * C * Wx * Wy * e, C, Wx, Wy, F, K, M,
+                           O + (size_t)n * M * Ho * Wo, precision, s);
+            if (st) return st;
+        }
+        return CONV_OK;
+    }
+    // TF32 / BF16: ONE launch of the implicit tensor-core kernel over all N images
+    return launch_status(launch_multi_tc(I, C, Wx, Wy, F, K, M, O, precision == CONV_BF16, s, N));
 }
 
 // ------------------------------------------------------------ host buffers
@@ -286,6 +312,17 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
     }
 }
 
+int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out) {
+    if (N < 1) return CONV_E_SHAPE;
+    int st = check_shape(C, Wx, Wy, K, M);
+    if (st) return st;
+    if (!out) return CONV_E_NULL;
+    if (precision == CONV_FP32 || N == 1) return conv_plan_multi(C, Wx, Wy, K, M, precision, out);
+    if (precision != CONV_TF32 && precision != CONV_BF16) return CONV_E_PRECISION;
+    plan_multi_tc(C, Wx, Wy, K, M, precision == CONV_BF16, nullptr, out, N);
+    return CONV_OK;
+}
+
 const char *conv_status_string(int status) {
     switch (status) {
         case CONV_OK: return "ok";
@@ -299,7 +336,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 2; }   // 1.2: + *_host_async
+int conv_version(void) { return (1 << 16) | 3; }   // 1.2: + *_host_async; 1.3: + batched
 
 }  // extern "C"
 

@@ -24,9 +24,10 @@ cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float
                               float *O, cudaStream_t s);
 
 // KM-TC: multi-channel tcgen05 implicit GEMM, TF32 or BF16 (conv_multi_tc.cu)
-int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p);
+// N > 1: a batch of N images, I [N][C][Wy][Wx], O [N][M][Ho][Wo] (shared F)
+int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p, int N = 1);
 cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
-                            float *O, bool bf16, cudaStream_t s);
+                            float *O, bool bf16, cudaStream_t s, int N = 1);
 
 // KM-TC/G: explicit im2col (L2-resident workspace) + TMA-fed tcgen05 GEMM
 // (conv_multi_gemm.cu).  plan returns nonzero / launch returns
@@ -36,7 +37,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
                               bool bf16, cudaStream_t s);
 
 // Split-K chooser: cluster size S (1..max_split) minimising
-//   waves(S) * ceil(units / S) * t_unit + (S > 1) * t_reduce,
+//   waves(S) * (ceil(units / S) * t_unit + (S > 1) * t_reduce),
 // waves(S) = ceil(tiles / clusters_resident(S)), with the co-resident cluster
 // counts MEASURED on B200 (cudaOccupancyMaxActiveClusters; tools/cluster_occ.py)
 // for kernels that fit 1 or 2 CTAs per SM.

@@ -22,11 +22,11 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 12
+    assert len(syms) == 14
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16) | 2
+    assert conv.version() == (1 << 16) | 3
 
 
 def test_status_strings():
@@ -118,3 +118,18 @@ def test_plans_cover_every_config_with_one_launch():
                 aligned = (cfg["C"] * cfg["K"] ** 2 * (2 if prec == "bf16" else 4)) % 16 == 0
                 assert (p["tma_f"] & 1) == int(aligned)        # bit 0: F tiles by TMA
                 assert p["tma_f"] & 2                            # bit 1: I patch by TMA
+
+
+def test_batched_plans():
+    # one launch over all N images: N times the pixel tiles, no split once N fills the SMs
+    for prec in ("tf32", "bf16"):
+        p1 = conv.plan_multi_batched(1, 256, 28, 28, 3, 256, prec)
+        p32 = conv.plan_multi_batched(32, 256, 28, 28, 3, 256, prec)
+        assert p32["kernel"] == 2 and p32["launches"] == 1
+        assert p32["grid_y"] == 32 * (-(-26 * 28 // 128))
+        assert p32["cluster_x"] == 1 and p1["kernel"] in (2, 3)
+    assert conv.plan_multi_batched(4, 16, 14, 14, 3, 32, "fp32")["kernel"] == 1
+    lib = conv.load()
+    f = 0x1000
+    assert lib.conv_multi_batched_ex(f, 0, 2, 8, 8, f, 3, 4, f, 1, None) == 1      # N < 1
+    assert lib.conv_multi_batched_ex(f, 1 << 20, 64, 64, 64, f, 3, 4, f, 1, None) == 1  # overflow

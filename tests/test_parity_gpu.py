@@ -317,3 +317,38 @@ def test_tc_paths_edges_and_ints(conv, monkeypatch, path, prec):
         I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
         Oo, _ = oracle.conv_multi(I, F)
         assert np.array_equal(run_multi(conv, I, F, prec), Oo), (C, W, K, M, prec, path)
+
+
+# ------------------------------------------------------------------ batched
+BATCHED = [  # (N, C, Wx, Wy, K, M): ragged pixel tiles, unaligned planes, split / no split
+    (4, 64, 14, 14, 3, 96), (3, 5, 17, 11, 3, 37), (2, 96, 27, 27, 5, 40), (8, 32, 28, 28, 3, 256),
+    (5, 130, 9, 9, 3, 33), (16, 16, 7, 7, 1, 20),
+]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("N,C,Wx,Wy,K,M", BATCHED)
+def test_batched_matches_oracle_per_image(conv, prec, N, C, Wx, Wy, K, M):
+    I = np.stack([synth.uniform01(50 + n, (C, Wy, Wx)) for n in range(N)])
+    F = synth.uniform_pm1(60, (M, C, K, K))
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    O = conv.multi_batched(torch.from_numpy(I).cuda().to(dt), torch.from_numpy(F).cuda().to(dt), prec)
+    torch.cuda.synchronize()
+    Og = O.cpu().numpy().astype(np.float64)
+    for n in range(N):
+        Oo, A = oracle.conv_multi(I[n], F)
+        assert_parity(Og[n], Oo, A, TAU[prec], f"batched n={n} {N},{C},{Wx},{Wy},{K},{M} {prec}")
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_batched_integer_bit_exact_and_equals_unbatched(conv, prec):
+    N, C, W, K, M = 6, 48, 20, 3, 136
+    I = np.stack([synth.layer_inputs(C, W, W, K, M, cfg_index=70 + n, kind="ints")[0] for n in range(N)])
+    F = synth.layer_inputs(C, W, W, K, M, cfg_index=70, kind="ints")[1]
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    Id, Fd = torch.from_numpy(I).cuda().to(dt), torch.from_numpy(F).cuda().to(dt)
+    Ob = conv.multi_batched(Id, Fd, prec).cpu().numpy()
+    for n in range(N):
+        Oo, _ = oracle.conv_multi(I[n], F)
+        assert np.array_equal(Ob[n].astype(np.float64), Oo), (n, prec)
+        assert np.array_equal(Ob[n], conv.multi(Id[n].contiguous(), Fd, prec).cpu().numpy()), (n, prec)
