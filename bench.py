@@ -342,6 +342,9 @@ def run_ours(args):
     # ---- strong scaling of the configs[4] sweep (M = 4096 split over the N ranks)
     strong = _strong_sweep(args, conv, dev, stream, world, rank, cacheI)
 
+    # ---- batched tensor-core path on the 28x28x256 layer
+    batched = _batched(args, conv, dev, stream, pk) if args.batched and rank == 0 else None
+
     # ---- cuDNN context on the same device / buffers
     cudnn = _cudnn_context(args, calls, dev, stream, capture, pk) if args.cudnn and rank == 0 else None
 
@@ -372,6 +375,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "strong_sweep": strong,
+        "batched": batched,
         "cudnn_context": cudnn,
         "clocks": clk.summary(),
         "paper_context": {"single_vs_cudnn71_avg": 2.6, "multi_vs_cudnn71_avg": 1.39,
@@ -435,6 +439,46 @@ def _traffic_lookup(kernel):
         return t.get(kernel)
     except Exception:
         return None
+
+
+def _batched(args, conv, dev, stream, pk):
+    """The north-star tensor-pipe layer (28x28, C = M = 256, K = 3) as CNNs run it:
+    a batch of N images in ONE launch (conv_multi_batched_ex), graph replay,
+    device events; tensor fraction against the measured peak (TF32 = bf16 / 2)."""
+    import torch
+    C, W, K, M = 256, 28, 3, 256
+    Ho = W - K + 1
+    out = {}
+    for prec in ("tf32", "bf16"):
+        dt = torch.bfloat16 if prec == "bf16" else torch.float32
+        peak = pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)
+        for N in (8, 32, 64):
+            I = torch.from_numpy(synth.uniform01(synth.SEED_I + N, (N, C, W, W))).to(dev, dt)
+            F = torch.from_numpy(synth.uniform_pm1(synth.SEED_F + N, (M, C, K, K))).to(dev, dt)
+            Os = [torch.empty((N, M, Ho, Ho), device=dev) for _ in range(3)]
+            g = torch.cuda.CUDAGraph()
+            reps = 10
+            with torch.cuda.stream(stream):
+                for j in range(3):
+                    conv.conv_multi_batched_ex(I, N, C, W, W, F, K, M, Os[j % 3], prec, stream.cuda_stream)
+                stream.synchronize()
+                g.capture_begin()
+                for j in range(reps):
+                    conv.conv_multi_batched_ex(I, N, C, W, W, F, K, M, Os[j % 3], prec, stream.cuda_stream)
+                g.capture_end()
+                g.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                stream.synchronize()
+            us = 1e3 * e0.elapsed_time(e1) / reps
+            tflops = 2.0 * N * M * C * K * K * Ho * Ho / (us * 1e-6) / 1e12
+            out[f"{prec}_n{N}"] = {"us": round(us, 2), "tflops": round(tflops, 1),
+                                   "tensor_frac": round(tflops / peak, 4),
+                                   "plan": conv.plan_multi_batched(N, C, W, W, K, M, prec)}
+    return out
 
 
 def _strong_sweep(args, conv, dev, stream, world, rank, cacheI):
@@ -689,6 +733,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-streams", type=int, default=8)
     ap.add_argument("--e2e-interleave", type=int, default=1)
+    ap.add_argument("--batched", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     args = ap.parse_args()

@@ -560,10 +560,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // filters per CTA tile (UMMA N).  N = 256 halves how often one im2col tile is
 // rebuilt (once per filter tile) when there are many filters.
-int tc_bn(int M) {
+// (pixel_tiles: 128-pixel tiles of the whole call.  N = 256 once there are
+// enough pixel tiles to fill the SMs without splitting k — one im2col build
+// per 256 filters: batched 28x28x256, N = 32: 105 vs 125 us TF32, 64 vs 84 us
+// BF16; single images keep N = 128 tiles and split k instead.)
+int tc_bn(int M, int pixel_tiles) {
+    if (const char *e = getenv("B200CONV_TC_BN")) {        // experiments: 32 / 64 / 128 / 256
+        const int v = atoi(e);
+        if (v == 32 || v == 64 || v == 128 || v == 256) return v;
+    }
     if (M <= 32) return 32;
     if (M <= 64) return 64;
-    if (M >= 1024) return 256;
+    if (M >= 1024 || (M >= 256 && pixel_tiles >= 64)) return 256;
     return 128;
 }
 }  // namespace
@@ -574,14 +582,21 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     const int BK = 128 / elem;
     const int64_t Ktot = (int64_t)C * K * K;
     const int nkb = (int)((Ktot + BK - 1) / BK);
-    const int BN = tc_bn(M);
     const int npt = N * ((Ho * Wx + kTcBM - 1) / kTcBM);   // pixel tiles of all N images
+    const int BN = tc_bn(M, npt);
     const int nft = (M + BN - 1) / BN;
     const int tiles = npt * nft;
     // split the k loop over a cluster (measured: ~0.45 us per k-block, ~3.5 us
     // for the partial-tile exchange through L2), at least 2 k-blocks per split
-    const int S = choose_split(tiles, nkb, nkb / 2 < kTcMaxSplit ? (nkb / 2 > 0 ? nkb / 2 : 1) : kTcMaxSplit,
-                               1, 0.45f, 3.5f);
+    // (no split once the tiles alone occupy most SMs: measured slower at every
+    // batched shape tried, e.g. 28x28x256 N=32 TF32 105 vs 94 us with S = 2)
+    int S = tiles >= 128 ? 1
+                         : choose_split(tiles, nkb, nkb / 2 < kTcMaxSplit ? (nkb / 2 > 0 ? nkb / 2 : 1) : kTcMaxSplit,
+                                        1, 0.45f, 3.5f);
+    if (const char *e = getenv("B200CONV_TC_SPLIT")) {     // experiments
+        const int v = atoi(e);
+        if (v >= 1 && v <= kTcMaxSplit && v <= nkb) S = v;
+    }
     const TcGeom gp = tc_geom(Wx, K, BN, elem, true);
     const bool patch = gp.stages >= 2;
     const TcGeom g = patch ? gp : tc_geom(Wx, K, BN, elem, false);
