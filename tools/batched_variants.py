@@ -3,6 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2212_00404_b200 import conv
+if os.environ.get("B200CONV_LIB_PATH"):           # A/B against another build of the library
+    conv.load(os.environ["B200CONV_LIB_PATH"])
 dev = torch.device("cuda"); s = torch.cuda.Stream()
 variants = sys.argv[1].split(";")
 N, C, W, K, M = (int(v) for v in sys.argv[2:7]); prec = sys.argv[7]
