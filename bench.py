@@ -478,6 +478,37 @@ def _batched(args, conv, dev, stream, pk):
             out[f"{prec}_n{N}"] = {"us": round(us, 2), "tflops": round(tflops, 1),
                                    "tensor_frac": round(tflops / peak, 4),
                                    "plan": conv.plan_multi_batched(N, C, W, W, K, M, prec)}
+    # the same layer as the networks define it: "same" 3x3 convolution (zero
+    # padding 1) — pad pre-pass + the batched kernel
+    for prec in ("fp32", "tf32", "bf16"):
+        dt = torch.bfloat16 if prec == "bf16" else torch.float32
+        for N in ((1,) if prec == "fp32" else (1, 32)):
+            I = torch.from_numpy(synth.uniform01(synth.SEED_I + 7 * N, (N, C, W, W))).to(dev, dt)
+            F = torch.from_numpy(synth.uniform_pm1(synth.SEED_F + 7 * N, (M, C, K, K))).to(dev, dt)
+            Os = [torch.empty((N, M, W, W), device=dev) for _ in range(3)]
+            g = torch.cuda.CUDAGraph()
+            reps = 10
+            with torch.cuda.stream(stream):
+                for j in range(3):
+                    conv.conv_multi_pad_ex(I, N, C, W, W, F, K, M, 1, Os[j % 3], prec, stream.cuda_stream)
+                stream.synchronize()
+                g.capture_begin()
+                for j in range(reps):
+                    conv.conv_multi_pad_ex(I, N, C, W, W, F, K, M, 1, Os[j % 3], prec, stream.cuda_stream)
+                g.capture_end()
+                g.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                stream.synchronize()
+            us = 1e3 * e0.elapsed_time(e1) / reps
+            tflops = 2.0 * N * M * C * K * K * W * W / (us * 1e-6) / 1e12
+            entry = {"us": round(us, 2), "tflops": round(tflops, 1)}
+            if prec != "fp32":
+                entry["tensor_frac"] = round(tflops / (pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)), 4)
+            out[f"{prec}_n{N}_pad1"] = entry
     return out
 
 

@@ -112,6 +112,19 @@ B200CONV_API int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void 
 B200CONV_API int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M,
                           float *O, int precision, void *stream);
 
+/* Zero ("same"-style) padding, stride 1: the input is
+ * read as if surrounded by `pad` zero rows / columns, so
+ * O [N][M][Wy+2*pad-K+1][Wx+2*pad-K+1].  A pre-pass kernel writes the padded
+ * copy of I into a library-owned per-stream buffer, then the same kernels as
+ * conv_single_ex / conv_multi_batched_ex run on it (one extra launch).
+ * pad == 0 is exactly the unpadded call.  pad < 0, N < 1 or a size overflow:
+ * CONV_E_SHAPE.  CONV_E_LAUNCH if the buffer would have to grow while the
+ * stream is being captured (run the shape once before capturing). */
+B200CONV_API int conv_single_pad_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, int pad, float *O,
+                       void *stream);
+B200CONV_API int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad,
+                      float *O, int precision, void *stream);
+
 /* End-to-end entry points on HOST buffers (pageable or pinned): copy I and F
  * host->device, run the same kernels as the *_ex calls, copy O device->host,
  * and synchronise the stream before returning.  Device scratch comes from a

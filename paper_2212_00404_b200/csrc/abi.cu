@@ -312,6 +312,46 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
     }
 }
 
+// ------------------------------------------------------------ zero padding
+int conv_single_pad_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, int pad, float *O,
+                       void *stream) {
+    if (pad < 0) return CONV_E_SHAPE;
+    if (pad == 0) return conv_single_ex(I, Wx, Wy, F, K, M, O, stream);
+    if (Wx < 1 || Wy < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
+        return CONV_E_SHAPE;
+    const int Wxp = Wx + 2 * pad, Wyp = Wy + 2 * pad;
+    int st = check_shape(1, Wxp, Wyp, K, M);
+    if (st) return st;
+    if ((st = check_ptrs(I, F, O, 4))) return st;
+    if ((st = check_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void *Ip = padbuf_get((size_t)Wxp * Wyp * 4, s);
+    if (!Ip) return CONV_E_LAUNCH;
+    if ((st = launch_status(launch_pad(I, 1, Wx, Wy, pad, 4, Ip, s)))) return st;
+    return launch_status(launch_single(static_cast<const float *>(Ip), Wxp, Wyp, F, K, M, O, s));
+}
+
+int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad, float *O,
+                      int precision, void *stream) {
+    if (pad < 0 || N < 1) return CONV_E_SHAPE;
+    if (pad == 0) return conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision, stream);
+    if (Wx < 1 || Wy < 1 || C < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
+        return CONV_E_SHAPE;
+    const int Wxp = Wx + 2 * pad, Wyp = Wy + 2 * pad;
+    int st = check_shape(C, Wxp, Wyp, K, M);
+    if (st) return st;
+    if ((int64_t)N * C * Wxp * Wyp > INT_MAX) return CONV_E_SHAPE;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    const int e = precision == CONV_BF16 ? 2 : 4;
+    if ((st = check_ptrs(I, F, O, e))) return st;
+    if ((st = check_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void *Ip = padbuf_get((size_t)N * C * Wxp * Wyp * e, s);
+    if (!Ip) return CONV_E_LAUNCH;
+    if ((st = launch_status(launch_pad(I, N * C, Wx, Wy, pad, e, Ip, s)))) return st;
+    return conv_multi_batched_ex(Ip, N, C, Wxp, Wyp, F, K, M, O, precision, stream);
+}
+
 int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out) {
     if (N < 1) return CONV_E_SHAPE;
     int st = check_shape(C, Wx, Wy, K, M);
@@ -336,7 +376,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 3; }   // 1.2: + *_host_async; 1.3: + batched
+int conv_version(void) { return (1 << 16) | 4; }   // 1.2: + *_host_async; 1.3: + batched; 1.4: + padding
 
 }  // extern "C"
 

@@ -50,6 +50,10 @@ int clusters_resident(int S, int ctas_per_sm);
 // library for (current device, stream); nullptr if it would have to grow
 // while the stream is being captured (or on OOM)
 void *workspace_get(size_t bytes, cudaStream_t s);
+// zero-padded input copies (padded calls): a second per-(device, stream) buffer
+void *padbuf_get(size_t bytes, cudaStream_t s);
+// Ip = I with a zero border of `pad` on every side of each of NC planes
+cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s);
 // O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
                                  cudaStream_t s);

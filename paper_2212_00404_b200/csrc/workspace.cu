@@ -21,6 +21,7 @@
 #include <mutex>
 #include <utility>
 #include <vector>
+#include <cuda_bf16.h>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -30,14 +31,23 @@ namespace {
 struct WsBuf { void *p = nullptr; size_t bytes = 0; };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
+std::map<std::pair<int, cudaStream_t>, WsBuf> g_pad;
 std::vector<void *> g_ws_retired;
 }  // namespace
 
-void *workspace_get(size_t bytes, cudaStream_t s) {
+static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, size_t bytes, cudaStream_t s);
+
+void *workspace_get(size_t bytes, cudaStream_t s) { return buffer_get(g_ws, bytes, s); }
+
+// The zero-padded copy of I for padded calls: a second per-(device, stream)
+// buffer, so the kernels of the same call can still use the workspace.
+void *padbuf_get(size_t bytes, cudaStream_t s) { return buffer_get(g_pad, bytes, s); }
+
+static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, size_t bytes, cudaStream_t s) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return nullptr; }
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    WsBuf &b = g_ws[{dev, s}];
+    WsBuf &b = pool[{dev, s}];
     if (b.bytes >= bytes) return b.p;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) { cudaGetLastError(); return nullptr; }
@@ -110,6 +120,45 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
                 if (n + i < N) o[i] = v[i];
         }
     }
+}
+
+// Ip[n][c][y][x] = I[n][c][y - pad][x - pad] inside, 0 in the border
+// (elem = 4 or 2 bytes; one element per thread, grid-stride).
+template <typename T>
+__global__ void __launch_bounds__(256)
+pad_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restrict__ Ip) {
+    pdl_wait();
+    pdl_trigger();
+    const int Wp = Wx + 2 * pad, Hp = Wy + 2 * pad;
+    const int64_t total = (int64_t)NC * Hp * Wp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t plane = i / ((int64_t)Hp * Wp);
+        const int rem = (int)(i - plane * Hp * Wp);
+        const int y = rem / Wp - pad, x = rem % Wp - pad;
+        T v = T(0.f);
+        if (y >= 0 && y < Wy && x >= 0 && x < Wx) v = I[(plane * Wy + y) * Wx + x];
+        Ip[i] = v;
+    }
+}
+
+cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s) {
+    const int64_t total = (int64_t)NC * (Wy + 2 * pad) * (Wx + 2 * pad);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (elem == 2)
+        return cudaLaunchKernelEx(&cfg, pad_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16 *>(I), NC, Wx,
+                                  Wy, pad, static_cast<__nv_bfloat16 *>(Ip));
+    return cudaLaunchKernelEx(&cfg, pad_kernel<float>, static_cast<const float *>(I), NC, Wx, Wy, pad,
+                              static_cast<float *>(Ip));
 }
 
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,

@@ -22,11 +22,11 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 14
+    assert len(syms) == 16
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16) | 3
+    assert conv.version() == (1 << 16) | 4
 
 
 def test_status_strings():
@@ -133,3 +133,14 @@ def test_batched_plans():
     f = 0x1000
     assert lib.conv_multi_batched_ex(f, 0, 2, 8, 8, f, 3, 4, f, 1, None) == 1      # N < 1
     assert lib.conv_multi_batched_ex(f, 1 << 20, 64, 64, 64, f, 3, 4, f, 1, None) == 1  # overflow
+
+
+def test_padded_argument_errors():
+    lib = conv.load()
+    f = 0x1000
+    assert lib.conv_multi_pad_ex(f, 1, 2, 8, 8, f, 3, 4, -1, f, 1, None) == 1        # pad < 0
+    assert lib.conv_multi_pad_ex(f, 0, 2, 8, 8, f, 3, 4, 1, f, 1, None) == 1         # N < 1
+    assert lib.conv_multi_pad_ex(f, 1, 2, 2, 2, f, 7, 4, 1, f, 1, None) == 1         # K > padded map
+    assert lib.conv_single_pad_ex(f, 8, 8, f, 3, 4, -2, f, None) == 1
+    assert lib.conv_single_pad_ex(0, 8, 8, f, 3, 4, 1, f, None) == 2                  # null
+    assert lib.conv_multi_pad_ex(f, 1, 2, 8, 8, f, 3, 4, 1, f, 9, None) == 4         # precision

@@ -352,3 +352,33 @@ def test_batched_integer_bit_exact_and_equals_unbatched(conv, prec):
         Oo, _ = oracle.conv_multi(I[n], F)
         assert np.array_equal(Ob[n].astype(np.float64), Oo), (n, prec)
         assert np.array_equal(Ob[n], conv.multi(Id[n].contiguous(), Fd, prec).cpu().numpy()), (n, prec)
+
+
+# ------------------------------------------------------------------ zero padding
+PADDED = [  # (N, C, Wx, Wy, K, M, pad): ResNet/VGG "same" 3x3 pad 1, AlexNet 5x5 pad 2, odd shapes
+    (1, 64, 14, 14, 3, 96, 1), (2, 96, 27, 27, 5, 64, 2), (3, 5, 9, 7, 3, 17, 1), (1, 3, 32, 32, 3, 64, 1),
+    (4, 32, 7, 7, 3, 128, 1), (1, 8, 4, 4, 7, 9, 3),
+]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("N,C,Wx,Wy,K,M,pad", PADDED)
+def test_padded_multi_matches_oracle_on_padded_input(conv, prec, N, C, Wx, Wy, K, M, pad):
+    I = np.stack([synth.uniform01(80 + n, (C, Wy, Wx)) for n in range(N)])
+    F = synth.uniform_pm1(90, (M, C, K, K))
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    O = conv.multi_padded(torch.from_numpy(I).cuda().to(dt), torch.from_numpy(F).cuda().to(dt), pad, prec)
+    Og = O.cpu().numpy().astype(np.float64)
+    for n in range(N):
+        Ip = np.pad(I[n], ((0, 0), (pad, pad), (pad, pad)))        # the definition of zero padding
+        Oo, A = oracle.conv_multi(Ip.astype(np.float32), F)
+        assert_parity(Og[n], Oo, A, TAU[prec], f"padded n={n} {C},{Wx},{Wy},{K},{M},p{pad} {prec}")
+
+
+@pytest.mark.parametrize("Wx,Wy,K,M,pad", [(28, 28, 3, 64, 1), (56, 56, 5, 32, 2), (7, 7, 7, 16, 3), (13, 9, 3, 5, 1)])
+def test_padded_single_matches_oracle_on_padded_input(conv, Wx, Wy, K, M, pad):
+    I = synth.uniform01(95, (Wy, Wx))
+    F = synth.uniform_pm1(96, (M, K, K))
+    Og = conv.single_padded(torch.from_numpy(I).cuda(), torch.from_numpy(F).cuda(), pad).cpu().numpy()
+    Oo, A = oracle.conv_single(np.pad(I, pad).astype(np.float32), F)
+    assert_parity(Og.astype(np.float64), Oo, A, TAU["fp32"], f"padded single p{pad}")
