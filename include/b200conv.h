@@ -25,12 +25,16 @@
  *
  * Ownership: every array pointer of the device entry points is a CUDA device
  * pointer owned by the caller; the library keeps no pointer after the call.
- * The only memory the library allocates is its split-K workspace: one device
- * buffer per (device, stream), grown on demand outside stream capture (the
- * growth synchronises that stream once) and kept for the process lifetime.
- * During stream capture a call never allocates: a shape whose workspace would
- * have to grow takes a cluster-only plan instead (same kernels).  The *_host entry points take host pointers and
- * manage their own stream-ordered device scratch.  O must not overlap I or F.
+ * The library allocates (i) its workspace — split-K partial tiles and the
+ * KM-TC/G im2col matrix — and (ii) the zero-padded input copy of the padded
+ * calls: one device buffer each per (device, stream), grown on demand outside
+ * stream capture (geometric growth; superseded buffers stay allocated, since
+ * a graph captured earlier may still reference them) and kept for the process
+ * lifetime.  During stream capture a call never allocates: a shape whose
+ * workspace would have to grow takes a plan that needs none (cluster / DSMEM
+ * reduction, implicit tensor-core kernel); a padded call returns
+ * CONV_E_LAUNCH.  The *_host entry points take host pointers and use a
+ * library-owned stream-ordered memory pool.  O must not overlap I or F.
  *
  * Execution: asynchronous and stream-ordered on the given stream (a
  * cudaStream_t / CUstream passed as void*; NULL = legacy default stream);
