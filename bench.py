@@ -81,26 +81,30 @@ def suite(world: int = 1, rank: int = 0, precisions=("fp32", "tf32", "bf16")):
         e = 2 if c["prec"] == "bf16" else 4
         c["bytes_alg"] = e * (c["C"] * c["Wx"] * c["Wy"] + c["M"] * c["C"] * c["K"] ** 2) \
             + 4 * c["M"] * c["Ho"] * c["Wo"]
-        c["kernel"] = {"single": "KS"}.get(c["kind"]) or ("KM-SIMT" if c["prec"] == "fp32" else
-                                                         f"{_tc_name(c)}-{c['prec']}")
+        c["kernel"] = {"single": "KS"}.get(c["kind"]) or _multi_name(c)
         c["label"] = f"{c['name']}:{c['prec']}"
     return calls
 
 
-def _tc_name(c):
-    """KM-TC (implicit kernel) or KM-TC/G (im2col + TMA GEMM pair), as planned."""
+def _multi_name(c):
+    """Kernel group of a multi-channel call, as planned: KS-C3 (RGB stems, any
+    precision), KM-SIMT (FP32), KM-TC (implicit) or KM-TC/G (im2col + GEMM)."""
     try:
         from paper_2212_00404_b200 import conv
-        p = conv.plan_multi(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], c["prec"])
-        return "KM-TC/G" if p["kernel"] == 3 else "KM-TC"
+        k = conv.plan_multi(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], c["prec"])["kernel"]
     except Exception:
-        return "KM-TC"
+        k = 1 if c["prec"] == "fp32" else 2
+    if k == 4:
+        return f"KS-C3-{c['prec']}"
+    if c["prec"] == "fp32":
+        return "KM-SIMT"
+    return f"{'KM-TC/G' if k == 3 else 'KM-TC'}-{c['prec']}"
 
 
 def roof_for(c, pk):
     """(bound, peak, unit, algorithmic amount per launch) of one call."""
     clk = pk["sm_max_mhz"] * 1e6
-    if c["kernel"] == "KS":
+    if c["kernel"] == "KS" or c["kernel"].startswith("KS-C3"):
         fp32_peak = NUM_SMS * FP32_LANES_PER_SM * 2 * clk / 1e12         # TFLOP/s
         t_hbm = c["bytes_alg"] / (pk["hbm_gbs"] * 1e9)
         t_alu = c["flop"] / (fp32_peak * 1e12)

@@ -158,7 +158,8 @@ B200CONV_API int conv_multi_host_async(const void *I, int C, int Wx, int Wy, con
  * (launches == 2: a deterministic fixed-order reduction kernel follows). */
 typedef struct {
     int kernel;        /* 0 = KS (single FP32), 1 = KM-SIMT (multi FP32), 2 = KM-TC implicit (tf32/bf16),
-                          3 = KM-TC/G: im2col kernel + TMA-fed tcgen05 GEMM (tf32/bf16) */
+                          3 = KM-TC/G: im2col kernel + TMA-fed tcgen05 GEMM (tf32/bf16),
+                          4 = KS-C3: channel-summing KS for C = 3, K = 3 / 5 layers (every precision) */
     int grid_x, grid_y, grid_z;
     int block_x;
     int cluster_x;     /* split-K factor over channels / K-blocks (1 = none) */

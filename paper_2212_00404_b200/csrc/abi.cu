@@ -83,6 +83,11 @@ int launch_status(cudaError_t e) {
 
 int run_multi(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
               int precision, cudaStream_t s) {
+    if (precision >= CONV_FP32 && precision <= CONV_BF16) {
+        const cudaError_t e = launch_multi_c3(I, C, Wx, Wy, F, K, M, O, precision == CONV_BF16, s);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+        cudaGetLastError();
+    }
     switch (precision) {
         case CONV_FP32:
             return launch_status(launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy,
@@ -298,6 +303,8 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (!out) return CONV_E_NULL;
+    if (precision >= CONV_FP32 && precision <= CONV_BF16 && plan_multi_c3(C, Wx, Wy, K, M, out) == 0)
+        return CONV_OK;
     switch (precision) {
         case CONV_FP32: plan_multi_simt(C, Wx, Wy, K, M, out); return CONV_OK;
         case CONV_TF32:

@@ -26,6 +26,8 @@
 //    aligned for any output offset.
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
+#include <cuda_bf16.h>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -40,8 +42,8 @@ __host__ __device__ constexpr int ks_min_blocks(int K) { return K >= 5 ? 2 : 3; 
 
 // Launch parameters of one KS call (computed by plan_ks on the host).
 struct KsArgs {
-    const float *I;
-    const float *F;
+    const void *I;    // float (or bf16 for the C = 3 variant)
+    const void *F;
     float *O;
     int Wx, Wy, M;
     int L;        // lane slots per output row: ceil(Wo / TX)
@@ -54,6 +56,7 @@ struct KsArgs {
     int gmax;     // filter-group capacity of the smem tap table
     int dbg;      // diagnostics: 1 = per-CTA globaltimer stamps into g_ks_stamps
     int prefetch; // L2 prefetch of the CTA's inputs before griddepcontrol.wait (B200CONV_PREFETCH=0: off)
+    int cstride;  // kC > 1: floats per staged channel in shared memory
 };
 
 // diagnostics (B200CONV_KS_DBG=1): per CTA [start, after griddepcontrol.wait,
@@ -95,11 +98,20 @@ __device__ __forceinline__ void stg_vec(float *p, const float *v) {
 // rg = s / L, column slot xv = s % L); its lane computes pixels x = TX*xv ..
 // x+TX-1 (the last slot of a row may be partial) of rows y0 .. y0+RR-1.
 // Loads are VL-wide (VL | Wx and the I alignment), stores VS-wide (VS | Wo).
-template <int K, int TX, int VL, int VS, int R, int RR>
-__global__ void __launch_bounds__(kKsThreads, ks_min_blocks(K))
+//
+// kC > 1 (the RGB stem layers, C = 3): the same kernel summing kC channels —
+// each CTA stages kC planes' rows (converted to f32; T = float or bf16) and
+// the lane's window loop runs over the channels (Eq. 1 with small C).
+template <typename T> __device__ __forceinline__ float to_f32(T v) { return static_cast<float>(v); }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <int K, int TX, int VL, int VS, int R, int RR, int kC = 1, typename T = float>
+__global__ void __launch_bounds__(kKsThreads, kC > 1 ? 2 : ks_min_blocks(K))
 ks_kernel(const KsArgs a) {
     constexpr int KK = K * K;
-    constexpr int GS = (R * KK + 3) & ~3;            // floats per filter group (16-B rows)
+    constexpr int CKK = kC * KK;                     // taps per filter
+    constexpr bool kPlain = kC == 1 && std::is_same<T, float>::value;
+    constexpr int GS = (R * CKK + 3) & ~3;           // floats per filter group (16-B rows)
     constexpr int NV = (TX + K - 1 + VL - 1) / VL;   // load vectors per window row
     extern __shared__ __align__(16) float smem[];
     const int Wx = a.Wx, Wy = a.Wy, M = a.M, L = a.L, NG = a.NG, nseg = a.nseg;
@@ -134,23 +146,26 @@ ks_kernel(const KsArgs a) {
     int gi = g - g_first;
     if (gi < 0) gi += NG;
 
+    const T *__restrict__ Ig = static_cast<const T *>(a.I);
+    const T *__restrict__ Fg = static_cast<const T *>(a.F);
     float *s_w = smem;                                // [gmax][GS]
-    float *s_in = smem + a.gmax * GS;                 // input rows [row_lo, row_hi), + pad
-    // s_in[pad + e - e0] = I[e]: smem and global agree mod 16 B
+    float *s_in = smem + a.gmax * GS;                 // input rows [row_lo, row_hi), + pad (per channel)
+    // s_in[pad + e - e0] = I[e]: smem and global agree mod 16 B (kC == 1)
     const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
-    const int pad = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3);
+    const int pad = kPlain ? (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3) : 0;
 
     // warm L2 with this CTA's input rows and taps while the previous kernel drains
     if (a.prefetch) {
-    for (int64_t e = e0 + 32 * tid; e < e1; e += 32 * kKsThreads) prefetch_l2(a.I + e);
+    for (int64_t e = e0 + 32 * tid; e < e1; e += 32 * kKsThreads) prefetch_l2(Ig + e);
     if (tid < ngr) {
         int g = g_first + tid;
         if (g >= NG) g -= NG;
-        prefetch_l2(a.F + (int64_t)g * R * KK);
+        prefetch_l2(Fg + (int64_t)g * R * CKK);
     }
     }
     pdl_wait();
     if (stamp) g_ks_stamps[4 * blockIdx.x + 1] = gtimer();
+    if constexpr (kPlain) {
     for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
         const int gi = idx / GS, e = idx - gi * GS;
         const int f = e / KK, t = e - f * KK;
@@ -158,7 +173,7 @@ ks_kernel(const KsArgs a) {
         if (g >= NG) g -= NG;
         const int m = g * R + f;
         const bool ok = f < R && m < M;
-        cp_async4(s_w + idx, ok ? a.F + (int64_t)m * KK + t : a.F, ok);
+        cp_async4(s_w + idx, ok ? Fg + (int64_t)m * KK + t : Fg, ok);
     }
     {
         const int nch = (int)((pad + (e1 - e0) + 3) >> 2);  // 16-B chunks of s_in
@@ -166,13 +181,44 @@ ks_kernel(const KsArgs a) {
             const int64_t e = e0 - pad + 4 * c;            // global element of the chunk's first float
             if (e >= e0 && e + 4 <= e1) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             ::"r"(smem_u32(s_in + 4 * c)), "l"(a.I + e) : "memory");
+                             ::"r"(smem_u32(s_in + 4 * c)), "l"(Ig + e) : "memory");
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const bool ok = e + i >= e0 && e + i < e1;
-                    cp_async4(s_in + 4 * c + i, ok ? a.I + e + i : a.I, ok);
+                    cp_async4(s_in + 4 * c + i, ok ? Ig + e + i : Ig, ok);
                 }
+            }
+        }
+    }
+    } else {
+        // kC channels (f32 or bf16) -> f32 shared copies, plain loads
+        for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
+            const int gi = idx / GS, e = idx - gi * GS;
+            const int f = e / CKK, t = e - f * CKK;
+            int g = g_first + gi;
+            if (g >= NG) g -= NG;
+            const int m = g * R + f;
+            s_w[idx] = (f < R && m < M) ? to_f32(Fg[(int64_t)m * CKK + t]) : 0.f;
+        }
+        const int64_t HWp = (int64_t)Wx * Wy;
+        const int n = (int)(e1 - e0);
+        // 16 independent loads in flight per thread (the staging is one
+        // global-latency round trip per batch, not per element)
+        constexpr int kUnr = 16;
+        for (int b0 = tid; b0 < kC * n; b0 += kKsThreads * kUnr) {
+            float v[kUnr];
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u) {
+                const int idx = b0 + u * kKsThreads;
+                const int c = idx / n, e = idx - c * n;
+                v[u] = idx < kC * n ? to_f32(Ig[c * HWp + e0 + e]) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u) {
+                const int idx = b0 + u * kKsThreads;
+                const int c = idx / n, e = idx - c * n;
+                if (idx < kC * n) s_in[c * a.cstride + e] = v[u];
             }
         }
     }
@@ -186,7 +232,7 @@ ks_kernel(const KsArgs a) {
 
     const float *sin = s_in + pad - (int64_t)row_lo * Wx;   // sin[y*Wx + x] = I[y][x]
     const int64_t plane = (int64_t)Ho * Wo;
-    float w[R * KK];
+    float w[R * CKK];
     bool need_w = true;
     for (int u = w0; u < w1; ++u) {
         const bool fine = a.dbg == 2 && blockIdx.x == 0 && threadIdx.x == 0 && u == w0;
@@ -195,12 +241,12 @@ ks_kernel(const KsArgs a) {
             need_w = false;
             const float *ws = s_w + gi * GS;
 #pragma unroll
-            for (int q = 0; q < (R * KK) / 4; ++q) {
+            for (int q = 0; q < (R * CKK) / 4; ++q) {
                 const float4 v = *reinterpret_cast<const float4 *>(ws + 4 * q);
                 w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
             }
 #pragma unroll
-            for (int q = (R * KK) & ~3; q < R * KK; ++q) w[q] = ws[q];
+            for (int q = (R * CKK) & ~3; q < R * CKK; ++q) w[q] = ws[q];
         }
         if (fine) g_ks_fine[1] = gtimer();
         const int y0 = rb * RB + rg * RR;
@@ -213,7 +259,9 @@ ks_kernel(const KsArgs a) {
                 for (int f = 0; f < R; ++f)
 #pragma unroll
                     for (int v = 0; v < TX; ++v) acc[q][f][v] = 0.f;
-            const float *base = sin + y0 * Wx + x;
+#pragma unroll
+            for (int ch = 0; ch < kC; ++ch) {
+            const float *base = sin + ch * a.cstride + y0 * Wx + x;
 #pragma unroll
             for (int ir = 0; ir < RR + K - 1; ++ir) {
                 float win[NV * VL];
@@ -231,9 +279,10 @@ ks_kernel(const KsArgs a) {
                             for (int f = 0; f < R; ++f)
 #pragma unroll
                                 for (int v = 0; v < TX; ++v)
-                                    acc[q][f][v] = fmaf(win[v + c], w[f * KK + r * K + c], acc[q][f][v]);
+                                    acc[q][f][v] = fmaf(win[v + c], w[f * CKK + ch * KK + r * K + c], acc[q][f][v]);
                         }
                     }
+            }
             }
             if (fine) g_ks_fine[2] = gtimer() + (unsigned long long)(acc[0][0][0] == 12345.f);
             float *of = a.O + ((int64_t)g * R * Ho + y0) * Wo + x;
@@ -319,6 +368,8 @@ namespace {
 __host__ __device__ constexpr int ks_TX(int K) { return K == 1 ? 4 : (K <= 3 ? 2 : 4); }
 __host__ __device__ constexpr int ks_R(int K) { return K <= 1 ? 8 : (K <= 3 ? 4 : 1); }
 __host__ __device__ constexpr int ks_RR(int K) { return K <= 1 ? 1 : (K <= 3 ? 2 : 4); }
+// filters per lane of the C = 3 variant (weights: R * 3 * K * K registers)
+__host__ __device__ constexpr int ks_R_c3(int K) { return K <= 3 ? 2 : 1; }
 
 struct KsPlan {
     KsArgs a;
@@ -328,8 +379,9 @@ struct KsPlan {
 bool al(const void *p, int bytes) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % bytes == 0; }
 
 // Max dynamic smem over the CTAs of a grid of G CTAs (filter taps + input rows).
-void ks_cta_needs(const KsArgs &a, int K, int R, int RR, int TX, int G, int *gmax, int *smem) {
-    const int KK = K * K, GS = (R * KK + 3) & ~3, RB = a.RWt * RR;
+void ks_cta_needs(const KsArgs &a, int K, int R, int RR, int TX, int G, int *gmax, int *smem, int kC,
+                  int *cstride) {
+    const int KK = K * K, GS = (R * kC * KK + 3) & ~3, RB = a.RWt * RR;
     int rows_max = 0, g = 1;
     for (int c = 0; c < G; ++c) {
         const int c0 = c * kKsWarps, c1 = c0 + kKsWarps;
@@ -342,12 +394,14 @@ void ks_cta_needs(const KsArgs &a, int K, int R, int RR, int TX, int G, int *gma
         if (rows > rows_max) rows_max = rows;
     }
     *gmax = g;
-    *smem = (g * GS + rows_max * a.Wx + 2 * TX + 8) * 4;
+    *cstride = (rows_max * a.Wx + 2 * TX + 8 + 3) & ~3;        // floats per staged channel
+    *smem = (g * GS + kC * *cstride) * 4;
 }
 
 // Returns false when the band kernel does not apply (K > 7 or the staged rows
 // of a CTA do not fit in shared memory).
-bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O, KsPlan *kp) {
+bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *O, KsPlan *kp, int kC = 1,
+             int elem = 4) {
     if (K > 7) return false;
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     // small maps with K >= 3: one row per lane (a multi-row register block
@@ -358,7 +412,7 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
     const char *sm = getenv("B200CONV_KS_SMALL");
     const int small_ho = sm ? atoi(sm) : (K == 3 ? 32 : 16);
     const bool small = K >= 3 && Ho <= small_ho;
-    const int TX = ks_TX(K), R = ks_R(K), RR = small ? 1 : ks_RR(K);
+    const int TX = ks_TX(K), R = kC > 1 ? ks_R_c3(K) : ks_R(K), RR = small ? 1 : ks_RR(K);
     KsArgs a = {};
     a.I = I; a.F = F; a.O = O;
     a.Wx = Wx; a.Wy = Wy; a.M = M;
@@ -390,8 +444,8 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
     // (K = 1, pure store stream: one CTA per SM measured fastest — 9.4 vs
     // 11.5 us for 224x224 M=256 — fewer warps per SM keep the store traffic
     // fairer across SMs; see tools/ks_variants.py)
-    const int cap = (K == 1 ? 1 : ks_min_blocks(K)) * kNumSMs;
-    const int max_smem = (ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
+    const int cap = (K == 1 ? 1 : (kC > 1 ? 2 : ks_min_blocks(K))) * kNumSMs;
+    const int max_smem = (kC == 1 && ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
     // (B200CONV_KS_SPREAD=1: at least one CTA per SM up to one unit per CTA;
     // measured neutral on the small maps, so off by default)
     int G = (a.U + kKsWarps - 1) / kKsWarps;
@@ -409,14 +463,16 @@ bool plan_ks(const float *I, int Wx, int Wy, const float *F, int K, int M, float
         a.ub = a.U / a.NW;
         a.ur = a.U - a.ub * a.NW;
         int smem;
-        ks_cta_needs(a, K, R, RR, TX, G, &a.gmax, &smem);
+        ks_cta_needs(a, K, R, RR, TX, G, &a.gmax, &smem, kC, &a.cstride);
         if (smem <= max_smem || G >= a.U) {
             if (smem > 200 * 1024) return false;
             kp->a = a;
             kp->RR = RR;
-            kp->VL = (Wx % TX == 0 && al(I, 4 * TX)) ? TX : 1;
+            kp->VL = (kC == 1 && elem == 4 && Wx % TX == 0 && al(I, 4 * TX)) ? TX : 1;
             kp->VS = (Wo % TX == 0 && al(O, 4 * TX)) ? TX : ((TX >= 2 && Wo % 2 == 0 && al(O, 8)) ? 2 : 1);
             if (RR != ks_RR(K)) kp->VL = kp->VS = 1;    // small-map variant: scalar loads / stores
+            // channel planes are staged from offset 0 of 16-B aligned regions
+            if (kC > 1) kp->VL = (Wx % TX == 0) ? TX : 1;
             kp->G = G;
             kp->smem = smem;
             return true;
@@ -503,6 +559,82 @@ static cudaError_t launch_ks_v(const KsPlan &kp, cudaStream_t s) {
     if (kp.VS == TX) return launch_ks<K, 1, TX>(kp, s);
     if (kp.VS == 2) return launch_ks<K, 1, V2>(kp, s);
     return launch_ks<K, 1, 1>(kp, s);
+}
+
+// ---------------------------------------------------------------- C = 3 (RGB stems)
+// The multi-channel layers with three input channels (VGG / AlexNet / ResNet
+// first layers) are output-store bound (C*K*K = 27 MACs per output) with too
+// little reduction for a GEMM: the channel-summing KS variant runs them for
+// every precision (TF32 inputs are consumed in full FP32 — more accurate than
+// the TF32 tolerance needs; BF16 inputs are widened to FP32).
+template <int K, int VL, int VS, typename T>
+static cudaError_t launch_ks_c3(const KsPlan &kp, cudaStream_t s) {
+    constexpr int RR = ks_RR(K);
+    auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R_c3(K), RR, 3, T>;
+    if (kp.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kp.G);
+    cfg.blockDim = dim3(kKsThreads);
+    cfg.dynamicSmemBytes = kp.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1] = {pdl_attr()};
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KsArgs a = kp.a;
+    a.dbg = 0;
+    a.prefetch = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int K, typename T>
+static cudaError_t launch_ks_c3_v(const KsPlan &kp, cudaStream_t s) {
+    constexpr int TX = ks_TX(K);
+    constexpr int V2 = TX >= 2 ? 2 : 1;
+    if (kp.VL == TX) {
+        if (kp.VS == TX) return launch_ks_c3<K, TX, TX, T>(kp, s);
+        if (kp.VS == 2) return launch_ks_c3<K, TX, V2, T>(kp, s);
+        return launch_ks_c3<K, TX, 1, T>(kp, s);
+    }
+    if (kp.VS == TX) return launch_ks_c3<K, 1, TX, T>(kp, s);
+    if (kp.VS == 2) return launch_ks_c3<K, 1, V2, T>(kp, s);
+    return launch_ks_c3<K, 1, 1, T>(kp, s);
+}
+
+static bool c3_applies(int C, int K, int Wy) {
+    const char *e = getenv("B200CONV_C3");
+    if (e && e[0] == '0') return false;
+    return C == 3 && (K == 3 || K == 5) && Wy - K + 1 > 16;   // (the 1-row small-map variant is not built)
+}
+
+int plan_multi_c3(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
+    if (!c3_applies(C, K, Wy)) return 1;
+    KsPlan kp;
+    if (!plan_ks(reinterpret_cast<const float *>(256), Wx, Wy, nullptr, K, M, reinterpret_cast<float *>(256), &kp, 3))
+        return 1;
+    p->kernel = 4;
+    p->block_x = kKsThreads;
+    p->grid_x = kp.G;
+    p->grid_y = 1;
+    p->grid_z = 1;
+    p->cluster_x = 1;
+    p->tile_m = ks_R_c3(K);                              // filters per task
+    p->tile_n = kp.a.RWt * kp.RR;                        // output rows per task (full width)
+    p->smem_bytes = kp.smem;
+    p->tma_f = 0;
+    p->launches = 1;
+    return 0;
+}
+
+cudaError_t launch_multi_c3(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                            bool bf16, cudaStream_t s) {
+    if (!c3_applies(C, K, Wy)) return cudaErrorNotSupported;
+    KsPlan kp;
+    if (!plan_ks(I, Wx, Wy, F, K, M, O, &kp, 3, bf16 ? 2 : 4) || kp.RR != ks_RR(K)) return cudaErrorNotSupported;
+    if (bf16) return K == 3 ? launch_ks_c3_v<3, __nv_bfloat16>(kp, s) : launch_ks_c3_v<5, __nv_bfloat16>(kp, s);
+    return K == 3 ? launch_ks_c3_v<3, float>(kp, s) : launch_ks_c3_v<5, float>(kp, s);
 }
 
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,

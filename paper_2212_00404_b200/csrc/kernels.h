@@ -18,6 +18,12 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p);
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                           cudaStream_t s);
 
+// KS-C3: the channel-summing KS variant for C = 3 (RGB stem) layers, every
+// precision (conv_single.cu); plan nonzero / cudaErrorNotSupported otherwise
+int plan_multi_c3(int C, int Wx, int Wy, int K, int M, conv_plan *p);
+cudaError_t launch_multi_c3(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                            bool bf16, cudaStream_t s);
+
 // KM-SIMT: multi-channel strict FP32 (conv_multi_simt.cu)
 int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p);
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
