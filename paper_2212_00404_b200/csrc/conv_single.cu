@@ -153,6 +153,9 @@ ks_kernel(const KsArgs a) {
     // s_in[pad + e - e0] = I[e]: smem and global agree mod 16 B (kC == 1)
     const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
     const int pad = kPlain ? (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3) : 0;
+    // bf16 rows can move as 4-B pairs when every channel's range starts 4-B aligned
+    const bool pairs_ok = !kPlain && sizeof(T) == 2 && ((int64_t)Wx * Wy) % 2 == 0 && e0 % 2 == 0 &&
+                          (reinterpret_cast<uintptr_t>(a.I) & 3) == 0 && ((e1 - e0) & 1) == 0;
 
     // warm L2 with this CTA's input rows and taps while the previous kernel drains
     if (a.prefetch) {
@@ -203,22 +206,34 @@ ks_kernel(const KsArgs a) {
         }
         const int64_t HWp = (int64_t)Wx * Wy;
         const int n = (int)(e1 - e0);
-        // 16 independent loads in flight per thread (the staging is one
-        // global-latency round trip per batch, not per element)
-        constexpr int kUnr = 16;
-        for (int b0 = tid; b0 < kC * n; b0 += kKsThreads * kUnr) {
-            float v[kUnr];
+        if constexpr (std::is_same<T, float>::value) {
+            // asynchronous 4-B copies, all in flight at once
+            for (int c = 0; c < kC; ++c)
+                for (int e = tid; e < n; e += kKsThreads)
+                    cp_async4(s_in + c * a.cstride + e, Ig + c * HWp + e0 + e, true);
+        } else if (pairs_ok) {
+            // bf16 pairs by 4-B copies into a raw area, widened after the wait
+            __nv_bfloat16 *raw = reinterpret_cast<__nv_bfloat16 *>(s_in + kC * a.cstride);
+            for (int c = 0; c < kC; ++c)
+                for (int e = 2 * tid; e < n; e += 2 * kKsThreads)
+                    cp_async4(raw + c * a.cstride + e, Ig + c * HWp + e0 + e, true);
+        } else {
+            // 16 independent loads in flight per thread
+            constexpr int kUnr = 16;
+            for (int b0 = tid; b0 < kC * n; b0 += kKsThreads * kUnr) {
+                float v[kUnr];
 #pragma unroll
-            for (int u = 0; u < kUnr; ++u) {
-                const int idx = b0 + u * kKsThreads;
-                const int c = idx / n, e = idx - c * n;
-                v[u] = idx < kC * n ? to_f32(Ig[c * HWp + e0 + e]) : 0.f;
-            }
+                for (int u = 0; u < kUnr; ++u) {
+                    const int idx = b0 + u * kKsThreads;
+                    const int c = idx / n, e = idx - c * n;
+                    v[u] = idx < kC * n ? to_f32(Ig[c * HWp + e0 + e]) : 0.f;
+                }
 #pragma unroll
-            for (int u = 0; u < kUnr; ++u) {
-                const int idx = b0 + u * kKsThreads;
-                const int c = idx / n, e = idx - c * n;
-                if (idx < kC * n) s_in[c * a.cstride + e] = v[u];
+                for (int u = 0; u < kUnr; ++u) {
+                    const int idx = b0 + u * kKsThreads;
+                    const int c = idx / n, e = idx - c * n;
+                    if (idx < kC * n) s_in[c * a.cstride + e] = v[u];
+                }
             }
         }
     }
@@ -226,6 +241,16 @@ ks_kernel(const KsArgs a) {
     pdl_trigger();
     cp_async_wait<0>();
     __syncthreads();
+    if constexpr (!kPlain && !std::is_same<T, float>::value) {
+        if (pairs_ok) {                              // widen the raw bf16 rows
+            const __nv_bfloat16 *raw = reinterpret_cast<const __nv_bfloat16 *>(s_in + kC * a.cstride);
+            const int n = (int)(e1 - e0);
+            for (int c = 0; c < kC; ++c)
+                for (int e = tid; e < n; e += kKsThreads)
+                    s_in[c * a.cstride + e] = __bfloat162float(raw[c * a.cstride + e]);
+            __syncthreads();
+        }
+    }
     if (stamp) g_ks_stamps[4 * blockIdx.x + 2] = gtimer();
 
     if (w0 >= w1 && !a.dbg) return;
@@ -464,6 +489,7 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
         a.ur = a.U - a.ub * a.NW;
         int smem;
         ks_cta_needs(a, K, R, RR, TX, G, &a.gmax, &smem, kC, &a.cstride);
+        if (kC > 1 && elem == 2) smem += kC * a.cstride * 2;     // raw bf16 rows before widening
         if (smem <= max_smem || G >= a.U) {
             if (smem > 200 * 1024) return false;
             kp->a = a;
@@ -584,7 +610,8 @@ static cudaError_t launch_ks_c3(const KsPlan &kp, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     KsArgs a = kp.a;
-    a.dbg = 0;
+    const char *dbg = getenv("B200CONV_KS_DBG");
+    a.dbg = dbg ? atoi(dbg) : 0;
     a.prefetch = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
