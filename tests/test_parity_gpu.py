@@ -382,3 +382,62 @@ def test_padded_single_matches_oracle_on_padded_input(conv, Wx, Wy, K, M, pad):
     Og = conv.single_padded(torch.from_numpy(I).cuda(), torch.from_numpy(F).cuda(), pad).cpu().numpy()
     Oo, A = oracle.conv_single(np.pad(I, pad).astype(np.float32), F)
     assert_parity(Og.astype(np.float64), Oo, A, TAU["fp32"], f"padded single p{pad}")
+
+
+# ------------------------------------------------------------------ determinism and stream capture
+# every kernel path: KS, KS-C3, KM-SIMT (cluster and workspace splits), KM-TC
+# (implicit, split / no split), KM-TC/G (filters on M, split), batched
+PATH_CASES = [  # (kind, C, W, K, M, prec)
+    ("single", 1, 224, 3, 64, "fp32"), ("multi", 3, 224, 3, 64, "bf16"), ("multi", 128, 28, 3, 128, "fp32"),
+    ("multi", 512, 7, 3, 512, "fp32"), ("multi", 256, 28, 3, 256, "tf32"), ("multi", 64, 56, 3, 64, "bf16"),
+    ("multi", 512, 7, 3, 512, "bf16"), ("multi", 512, 14, 3, 1024, "tf32"),
+]
+
+
+def _case_tensors(kind, C, W, K, M, prec, seed):
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    I = torch.from_numpy(synth.uniform01(seed, (C, W, W))).cuda().to(dt)
+    F = torch.from_numpy(synth.uniform_pm1(seed + 1, (M, C, K, K))).cuda().to(dt)
+    if kind == "single":
+        I, F = I[0].contiguous(), F[:, 0].contiguous()
+    O = torch.empty((M, W - K + 1, W - K + 1), device="cuda")
+    return I, F, O
+
+
+def _call(conv, kind, I, F, O, C, W, K, M, prec, stream):
+    if kind == "single":
+        conv.conv_single_ex(I, W, W, F, K, M, O, stream)
+    else:
+        conv.conv_multi_ex(I, C, W, W, F, K, M, O, prec, stream)
+
+
+def test_every_path_is_run_to_run_deterministic(conv):
+    for i, (kind, C, W, K, M, prec) in enumerate(PATH_CASES):
+        I, F, O = _case_tensors(kind, C, W, K, M, prec, 300 + 2 * i)
+        outs = []
+        for _ in range(3):
+            O.fill_(float("nan"))
+            _call(conv, kind, I, F, O, C, W, K, M, prec, None)
+            torch.cuda.synchronize()
+            outs.append(O.cpu().numpy().copy())
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), (kind, C, W, K, M, prec)
+
+
+def test_every_path_replays_from_a_cuda_graph(conv):
+    # capture after a warm-up call (workspaces exist), replay, compare with eager
+    s = torch.cuda.Stream()
+    for i, (kind, C, W, K, M, prec) in enumerate(PATH_CASES):
+        I, F, O = _case_tensors(kind, C, W, K, M, prec, 400 + 2 * i)
+        with torch.cuda.stream(s):
+            _call(conv, kind, I, F, O, C, W, K, M, prec, s.cuda_stream)
+            s.synchronize()
+            ref = O.clone()
+            O.fill_(float("nan"))
+            g = torch.cuda.CUDAGraph()
+            g.capture_begin()
+            _call(conv, kind, I, F, O, C, W, K, M, prec, s.cuda_stream)
+            g.capture_end()
+            g.replay()
+            g.replay()
+            s.synchronize()
+        assert torch.equal(O, ref), (kind, C, W, K, M, prec)
