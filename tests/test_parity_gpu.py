@@ -441,3 +441,19 @@ def test_every_path_replays_from_a_cuda_graph(conv):
             g.replay()
             s.synchronize()
         assert torch.equal(O, ref), (kind, C, W, K, M, prec)
+
+
+# ------------------------------------------------------------------ KS-C3 (C = 3 stems): odd shapes
+C3_CASES = [  # (Wx, Wy, K, M): odd planes (BF16 element staging), K = 5, ragged filter groups
+    (33, 29, 3, 7), (40, 40, 5, 64), (27, 31, 5, 9), (224, 19, 3, 130), (57, 57, 3, 1),
+]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("Wx,Wy,K,M", C3_CASES)
+def test_c3_stem_path_matches_oracle(conv, prec, Wx, Wy, K, M):
+    assert conv.plan_multi(3, Wx, Wy, K, M, prec)["kernel"] == 4
+    I = synth.uniform01(500 + Wx, (3, Wy, Wx))
+    F = synth.uniform_pm1(600 + K, (M, 3, K, K))
+    Oo, A = oracle.conv_multi(I, F)
+    assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"c3 {Wx}x{Wy} K{K} M{M} {prec}")
