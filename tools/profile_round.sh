@@ -23,3 +23,6 @@ echo "full ks rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 \
     -o gpurun_out/full_tcg_$R python tools/run_layer.py sweep_14x14_c512_m4096_k3:bf16 3 > /dev/null 2>&1
 echo "full tcg rc=$?"
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:kmtc_kernel -s 2 -c 1 \
+    -o gpurun_out/full_tcbatched_$R python tools/run_batched.py 64 tf32 3 > /dev/null 2>&1
+echo "full tc batched rc=$?"
