@@ -308,15 +308,17 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
         const int h = gt >> 7;                           // which half of the 128-B row
         const int p = p0 + g;
         const bool prow = p < Ho * Wx;
-        for (int i = 0; i < niter; ++i) {
-            const int s = i % NS;
+        // stage / parity / first channel of the k-block advanced incrementally
+        // (no integer division per k-block on the gather warps)
+        int ch_lo = (kb0 * BK) / KK;
+        for (int i = 0, s = 0, ph = 0, k0 = kb0 * BK; i < niter;
+             ++i, k0 += BK, (++s == NS) ? (s = 0, ph ^= 1) : 0) {
             uint8_t *a_s = smem + s * STAGE;
-            const int k0 = (kb0 + i) * BK;
-            const int ch_lo = k0 / KK;
+            while ((ch_lo + 1) * KK <= k0) ++ch_lo;
             // stage free (non-patch path) / patch landed (patch path; the producer
             // only loads it after the MMA released the stage)
-            if (kPatch) wait(&pfull[s], (i / NS) & 1);
-            else wait(&empty[s], ((i / NS) & 1) ^ 1);
+            if (kPatch) wait(&pfull[s], (uint32_t)ph);
+            else wait(&empty[s], (uint32_t)(ph ^ 1));
             if (dbg & 1) {
                 if (!(dbg & 32)) fence_proxy_async_smem();
                 __syncwarp();
