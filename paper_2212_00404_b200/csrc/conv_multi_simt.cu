@@ -153,51 +153,65 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int by = bvalid ? bo / Wo : 0;
     const int bbase = by * Wx + (bvalid ? bo - by * Wo : 0);
 
+    // F rows: thread -> fixed vector column v of rows mr, mr + rpt, ... (chunk
+    // invariant, decoded once)
+    const int f_nv = CK / vw;
+    const int f_rpt = NT / f_nv;
+    const bool f_act = tid < f_nv * f_rpt;
+    const int f_v = f_act ? tid % f_nv : 0, f_mr = f_act ? tid / f_nv : 0;
+    const uint32_t f_dst0 = smem_u32(Fraw + f_mr * RS + vw * f_v);
+    const int64_t f_src0 = (int64_t)(m0 + f_mr) * Ktot + vw * f_v;
     auto load_f = [&](int chunk) {
+        if (!f_act) return;
         const int ch0 = ch_begin + chunk * CB;
         const int nk = min(CB, ch_end - ch0) * KK;            // valid k of this chunk
-        const float *fbase = F + (int64_t)m0 * Ktot + (int64_t)ch0 * KK;
-        // thread -> fixed vector column v of rows mr, mr + rpt, ...: no division in the loop
-        const int nv = CK / vw;
-        const int rpt = NT / nv;
-        if (tid < nv * rpt) {
-            const int v = tid % nv, mr = tid / nv;
-            const bool kok = vw * v < nk;                     // nk is a multiple of vw
-            const float *src = fbase + (int64_t)mr * Ktot + vw * v;
-            uint32_t dst = smem_u32(Fraw + mr * RS + vw * v);
-            for (int m = mr; m < BM; m += rpt) {
-                const bool ok = kok && (m0 + m < M);
-                const float *sp = ok ? src : F;
-                if (vw == 4)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
-                                 ::"r"(dst), "l"(sp), "r"(ok ? 16 : 0) : "memory");
-                else if (vw == 2)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
-                                 ::"r"(dst), "l"(sp), "r"(ok ? 8 : 0) : "memory");
-                else
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
-                                 ::"r"(dst), "l"(sp), "r"(ok ? 4 : 0) : "memory");
-                src += (int64_t)rpt * Ktot;
-                dst += rpt * RS * 4;
-            }
+        const bool kok = vw * f_v < nk;                       // nk is a multiple of vw
+        const float *src = F + f_src0 + (int64_t)ch0 * KK;
+        uint32_t dst = f_dst0;
+        for (int m = f_mr; m < BM; m += f_rpt) {
+            const bool ok = kok && (m0 + m < M);
+            const float *sp = ok ? src : F;
+            if (vw == 4)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                             ::"r"(dst), "l"(sp), "r"(ok ? 16 : 0) : "memory");
+            else if (vw == 2)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                             ::"r"(dst), "l"(sp), "r"(ok ? 8 : 0) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                             ::"r"(dst), "l"(sp), "r"(ok ? 4 : 0) : "memory");
+            src += (int64_t)f_rpt * Ktot;
+            dst += f_rpt * RS * 4;
         }
     };
     // im2col tile B[k][n] = I[ch0 + ch][y_n + r][x_n + c] (zero past the valid range)
     auto load_b = [&](int chunk, int b) {
         if (bkl >= KL) return;
         const int ch0 = ch_begin + chunk * CB;
-        const int nk = min(CB, ch_end - ch0) * KK;
+        const int nk = bvalid ? min(CB, ch_end - ch0) * KK : 0;
         const float *src = I + (int64_t)ch0 * HW + bbase;
-        float *dst = Bs_buf + b * CK * BN + bn;
-        for (int k = bkl; k < CK; k += KL) {
-            const bool ok = bvalid && k < nk;
-            cp_async4(dst + k * BN, ok ? src + koff[k] : I, ok);
-        }
+        uint32_t dst = smem_u32(Bs_buf + b * CK * BN + bkl * BN + bn);
+#pragma unroll 4
+        for (int k = bkl; k < CK; k += KL, dst += KL * BN * 4)
+            cp_async4_zf(dst, src + koff[k], k < nk);    // k >= nk: zero fill, src not read
     };
     // Fraw[m][k..k+3] (16-B loads along m: RS == 4 mod 32 -> conflict-free)
     //   -> F_s[k+i][m] (scalar stores, consecutive m -> conflict-free)
     auto transpose_f = [&]() {
         float *fs = Fs_buf;
+        if (CK % 4 == 0) {
+            // thread -> fixed m, quads q0, q0 + QS, ...: pointer increments only
+            constexpr int QS = NT / BM;
+            const int m = tid % BM, q0 = tid / BM;
+            const float *src = Fraw + m * RS + 4 * q0;
+            float *dst = fs + 4 * q0 * BM + m;
+#pragma unroll 4
+            for (int q = q0; q < CK / 4; q += QS, src += 4 * QS, dst += 4 * QS * BM) {
+                const float4 v = *reinterpret_cast<const float4 *>(src);
+                dst[0] = v.x; dst[BM] = v.y; dst[2 * BM] = v.z; dst[3 * BM] = v.w;
+            }
+            return;
+        }
         const int nq = (CK + 3) / 4;
         for (int u = tid; u < BM * nq; u += NT) {
             const int m = u % BM, q = u / BM;

@@ -230,6 +230,13 @@ __device__ __forceinline__ void cp_async4(void *dst, const void *src, bool pred)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(pred ? 4 : 0) : "memory");  // 0 -> zero fill
 }
+// 4-B cp.async to a shared::cta address; !pred -> zero fill, src not read
+// (the ignore-src form: no src-size arithmetic around the LDGSTS)
+__device__ __forceinline__ void cp_async4_zf(uint32_t dst, const void *src, bool pred) {
+    asm volatile("{\n .reg .pred q;\n setp.eq.u32 q, %2, 0;\n"
+                 " cp.async.ca.shared.global [%0], [%1], 4, q;\n}"
+                 ::"r"(dst), "l"(src), "r"((uint32_t)pred) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }

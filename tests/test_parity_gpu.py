@@ -319,6 +319,25 @@ def test_tc_paths_edges_and_ints(conv, monkeypatch, path, prec):
         assert np.array_equal(run_multi(conv, I, F, prec), Oo), (C, W, K, M, prec, path)
 
 
+# KM-SIMT: every thread tile (B200CONV_SIMT_FORCE="tile,split,ws"), with no
+# split, a cluster (DSMEM) split and a workspace split; shapes with chunks of
+# k-steps that are / are not multiples of 4 (both F-transpose loops), ragged
+# pixel and filter tiles, unaligned F rows (C*K*K odd).
+SIMT_SHAPES = [(64, 14, 14, 3, 96), (20, 17, 11, 3, 70), (7, 9, 12, 5, 33), (130, 9, 9, 3, 300)]
+
+
+@pytest.mark.parametrize("tile", range(9))
+@pytest.mark.parametrize("split,ws", [(1, 0), (3, 0), (5, 1)])
+def test_simt_every_tile_and_split(conv, monkeypatch, tile, split, ws):
+    monkeypatch.setenv("B200CONV_SIMT_FORCE", f"{tile},{split},{ws}")
+    for (C, Wx, Wy, K, M) in SIMT_SHAPES:
+        I = synth.uniform01(41, (C, Wy, Wx))
+        F = synth.uniform_pm1(42, (M, C, K, K))
+        Oo, A = oracle.conv_multi(I, F)
+        assert_parity(run_multi(conv, I, F, "fp32"), Oo, A, TAU["fp32"],
+                      f"simt tile {tile} split {split} ws {ws} shape {(C, Wx, Wy, K, M)}")
+
+
 # ------------------------------------------------------------------ batched
 BATCHED = [  # (N, C, Wx, Wy, K, M): ragged pixel tiles, unaligned planes, split / no split
     (4, 64, 14, 14, 3, 96), (3, 5, 17, 11, 3, 37), (2, 96, 27, 27, 5, 40), (8, 32, 28, 28, 3, 256),
