@@ -17,8 +17,9 @@ full-size slice of a global problem with N*M filters, so per-GPU work is fixed
 I is broadcast once at setup over NCCL.  The strong-scaling numbers of the
 configs[4] sweep (M = 4096 split N ways) are reported in "strong_sweep".
 
-Timing: W warm-up steps; the step is captured in CUDA graphs (one kernel launch
-per layer, event-record nodes between layers); K steps replayed back to back
+Timing: W warm-up steps; the step is captured in ONE CUDA graph (one call per
+layer, PDL-chained; the per-group breakdown is the time the step loses
+without each group); K steps replayed back to back
 between a barrier + synchronize on both sides; device time from CUDA events;
 max over ranks.  The step's working set (>1.5 GB) is far larger than the
 126 MB L2, so every layer's buffers are evicted by the rest of the step before
@@ -254,8 +255,8 @@ def run_ours(args):
                 launch(c)
     stream.synchronize()
 
-    # ---- the step as CUDA graphs, one per (kernel, binding roof) group; the
-    # groups are timed live with stream events between graph replays
+    # ---- the step grouped by (kernel, binding roof); each group is timed live
+    # as the difference between the step and the step without it (below)
     order = []
     for c in calls:
         c["bound"] = roof_for(c, pk)[0]
@@ -274,18 +275,21 @@ def run_ours(args):
         return g
 
     # the whole step as ONE graph (every layer PDL-chained to the next) for the
-    # timed region; one graph per group for the per-group breakdown below
+    # timed region; for the per-group breakdown below, the step without each
+    # group in turn (a group's time = what removing it saves: its share of the
+    # PDL-chained step, with no event or graph boundary around it)
     step_graph = capture(lambda: [launch(c) for _key, cs in groups for c in cs])
-    graphs = [capture(lambda cs=cs: [launch(c) for c in cs]) for _key, cs in groups]
+    G = len(groups)
+    minus_graphs = [capture(lambda gi=gi: [launch(c) for gj, (_key, cs) in enumerate(groups) if gj != gi
+                                           for c in cs]) for gi in range(G)]
     with torch.cuda.stream(stream):
         for _ in range(max(1, args.warmup)):
             step_graph.replay()
-            for g in graphs:
+            for g in minus_graphs:
                 g.replay()
     torch.cuda.synchronize()
 
     # ---- timed region: exactly K steps
-    G = len(graphs)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -303,16 +307,24 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
-    # per-group breakdown (outside the timed region): each group's graph alone,
-    # K replays of the group sequence with events between the groups
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(G + 1)] for _ in range(args.steps)]
-    with torch.cuda.stream(stream):
-        for s in range(args.steps):
-            for gi, g in enumerate(graphs):
-                evs[s][gi].record(stream)
-                g.replay()
-            evs[s][G].record(stream)
+    # per-group breakdown (outside the timed region): R replays of the full
+    # step and of each step-minus-group graph, interleaved in 4 rounds
+    R = max(20, min(args.steps, 100))
+
+    def _replays_us(g):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(R):
+            g.replay()
+        b.record(stream)
         stream.synchronize()
+        return 1e3 * a.elapsed_time(b) / R
+    full_s, minus_s = [], [[] for _ in range(G)]
+    with torch.cuda.stream(stream):
+        for _round in range(4):
+            full_s.append(_replays_us(step_graph))
+            for gi in range(G):
+                minus_s[gi].append(_replays_us(minus_graphs[gi]))
     if world > 1:
         tt = torch.tensor([total_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -322,8 +334,8 @@ def run_ours(args):
     value = world * flop_rank / (ms_per_step * 1e-3) / 1e9
 
     # ---- per-group (kernel x roof) live timing -> roofline of the dominant kernel
-    gus = [statistics.median(1e3 * evs[s][gi].elapsed_time(evs[s][gi + 1]) for s in range(args.steps))
-           for gi in range(G)]
+    full_us = statistics.median(full_s)
+    gus = [max(full_us - statistics.median(minus_s[gi]), 1e-3) for gi in range(G)]
     step_us_sum = sum(gus)
     kernels = {}
     for (key, cs), us in zip(groups, gus):
