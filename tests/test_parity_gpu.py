@@ -338,6 +338,23 @@ def test_simt_every_tile_and_split(conv, monkeypatch, tile, split, ws):
                       f"simt tile {tile} split {split} ws {ws} shape {(C, Wx, Wy, K, M)}")
 
 
+# KM-TC implicit kernel with every filter-tile width (B200CONV_TC_BN) and a
+# forced k split, on shapes with ragged filter / pixel tiles
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_tc_every_filter_tile_width(conv, monkeypatch, bn, prec):
+    monkeypatch.setenv("B200CONV_GM", "0")
+    monkeypatch.setenv("B200CONV_TC_BN", str(bn))
+    for split in ("1", "3"):
+        monkeypatch.setenv("B200CONV_TC_SPLIT", split)
+        for (C, Wx, Wy, K, M) in [(64, 14, 14, 3, 300), (20, 17, 11, 3, 70), (48, 30, 30, 5, 40)]:
+            I = synth.uniform01(43, (C, Wy, Wx))
+            F = synth.uniform_pm1(44, (M, C, K, K))
+            Oo, A = oracle.conv_multi(I, F)
+            assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec],
+                          f"tc BN {bn} split {split} {prec} shape {(C, Wx, Wy, K, M)}")
+
+
 # ------------------------------------------------------------------ batched
 BATCHED = [  # (N, C, Wx, Wy, K, M): ragged pixel tiles, unaligned planes, split / no split
     (4, 64, 14, 14, 3, 96), (3, 5, 17, 11, 3, 37), (2, 96, 27, 27, 5, 40), (8, 32, 28, 28, 3, 256),
