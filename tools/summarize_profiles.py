@@ -61,11 +61,29 @@ with open(os.path.join(ROOT, "profiles", f"launches_{r}.csv"), "w", newline="") 
 tot = sum(g["us"] for g in groups.values())
 traffic = {k: int(g["traffic"] / g["n"]) for k, g in groups.items()}
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+# the bench's live per-group shares (profiles/bench_<r>.json), side by side
+live = {}
+bj = os.path.join(ROOT, "profiles", f"bench_{r}.json")
+if os.path.exists(bj):
+    live = {k: v["share"] for k, v in json.load(open(bj)).get("kernels", {}).items()}
+big = [k for k, g in groups.items() if g["us"] / g["n"] >= 8.0]          # launches well above the launch floor
+tot_big = sum(groups[k]["us"] for k in big)
+live_big = sum(live.get(k, 0.0) for k in big)
 with open(os.path.join(ROOT, "profiles", f"launch_shares_{r}.txt"), "w") as fh:
     fh.write(f"# ncu launch list of one bench step ({len(out_rows)} launches), cold-cache + serialised\n")
-    fh.write(f"# {'group':24s} {'launches':>8s} {'ncu us':>10s} {'share':>7s} {'dram/launch':>12s} {'alg/launch':>12s}\n")
+    fh.write("# 'live' = the bench's share of the PDL-chained step (bench_<r>.json).  ncu serialises\n"
+             "# launches and flushes caches, so tiny launches (KS on 7-56 px maps: ~2 us live) cost\n"
+             "# 5-7 us each here; among groups averaging >= 8 us per ncu launch the shares are\n"
+             "# compared renormalised over those groups ('ncu big' vs 'live big').\n")
+    fh.write(f"# {'group':24s} {'launches':>8s} {'ncu us':>10s} {'share':>7s} {'live':>7s} {'ncu big':>8s} {'live big':>8s}"
+             f" {'dram/launch':>12s} {'alg/launch':>12s}\n")
     for k, g in sorted(groups.items(), key=lambda kv: -kv[1]["us"]):
-        fh.write(f"  {k:24s} {g['n']:8d} {g['us']:10.1f} {g['us'] / tot:7.3f} {g['traffic'] / g['n']:12.0f} {g['alg'] / g['n']:12.0f}\n")
+        lv = live.get(k)
+        nb = f"{g['us'] / tot_big:8.3f}" if k in big and tot_big else f"{'':8s}"
+        lb = f"{lv / live_big:8.3f}" if k in big and lv is not None and live_big else f"{'':8s}"
+        fh.write(f"  {k:24s} {g['n']:8d} {g['us']:10.1f} {g['us'] / tot:7.3f} "
+                 f"{(f'{lv:7.3f}' if lv is not None else ' ' * 7)} {nb} {lb} "
+                 f"{g['traffic'] / g['n']:12.0f} {g['alg'] / g['n']:12.0f}\n")
 print(open(os.path.join(ROOT, "profiles", f"launch_shares_{r}.txt")).read())
 for f in sorted(os.listdir(os.path.join(ROOT, "gpurun_out"))):
     if f.startswith("full_") and f.endswith(f"_{r}.ncu-rep"):
