@@ -535,6 +535,43 @@ def _batched(args, conv, dev, stream, pk):
             if prec != "fp32":
                 entry["tensor_frac"] = round(tflops / (pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)), 4)
             out[f"{prec}_n{N}_pad1"] = entry
+    # stride 2: the ResNet downsampling 3x3 convolution,
+    # 56x56x64 -> 28x28x128, pad 1 (conv_multi_strided_ex; per image)
+    C2, W2, K2, M2, P2, S2 = 64, 56, 3, 128, 1, 2
+    Ho2 = (W2 + 2 * P2 - K2) // S2 + 1
+    for prec in ("fp32", "tf32", "bf16"):
+        dt = torch.bfloat16 if prec == "bf16" else torch.float32
+        for N in (1, 8):
+            I = torch.from_numpy(synth.uniform01(synth.SEED_I + 11 * N, (N, C2, W2, W2))).to(dev, dt)
+            F = torch.from_numpy(synth.uniform_pm1(synth.SEED_F + 11 * N, (M2, C2, K2, K2))).to(dev, dt)
+            Os = [torch.empty((N, M2, Ho2, Ho2), device=dev) for _ in range(3)]
+            g = torch.cuda.CUDAGraph()
+            reps = 10
+            with torch.cuda.stream(stream):
+                for j in range(3):
+                    conv.conv_multi_strided_ex(I, N, C2, W2, W2, F, K2, M2, P2, S2, Os[j % 3], prec,
+                                               stream.cuda_stream)
+                stream.synchronize()
+                g.capture_begin()
+                for j in range(reps):
+                    conv.conv_multi_strided_ex(I, N, C2, W2, W2, F, K2, M2, P2, S2, Os[j % 3], prec,
+                                               stream.cuda_stream)
+                g.capture_end()
+                g.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                stream.synchronize()
+            us = 1e3 * e0.elapsed_time(e1) / reps
+            tflops = 2.0 * N * M2 * C2 * K2 * K2 * Ho2 * Ho2 / (us * 1e-6) / 1e12
+            entry = {"us": round(us, 2), "tflops": round(tflops, 1),
+                     "layer": "56x56x64 -> 28x28x128, 3x3, stride 2, pad 1",
+                     "plan": conv.plan_multi_strided(C2, W2, W2, K2, M2, P2, S2, prec, N)}
+            if prec != "fp32":
+                entry["tensor_frac"] = round(tflops / (pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)), 4)
+            out[f"{prec}_n{N}_s2"] = entry
     return out
 
 

@@ -129,6 +129,25 @@ B200CONV_API int conv_single_pad_ex(const float *I, int Wx, int Wy, const float 
 B200CONV_API int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad,
                       float *O, int precision, void *stream);
 
+/* Stride (PAPER.md treats stride 1 only): output
+ * pixel (y, x) is the window at input (y*stride, x*stride) of the zero-padded
+ * input, so O [N][M][Ho][Wo] with Ho = (Wy+2*pad-K)/stride+1 and
+ * Wo = (Wx+2*pad-K)/stride+1 (torch.nn.functional.conv2d(I, F, stride=stride,
+ * padding=pad)).  stride == 1 is exactly conv_*_pad_ex.  stride > 1:
+ *   CONV_FP32  KM-SIMT with strided im2col gathers, one launch (+ split-K
+ *              reduce) per image;
+ *   CONV_TF32 / CONV_BF16  KM-TC/G: the strided im2col of all N images into
+ *              the workspace, then ONE TMA-fed tcgen05 GEMM; filter rows that are not 16-B
+ *              strided are first copied to zero-padded rows in a third
+ *              library-owned per-stream buffer (one extra launch).
+ * conv_single_strided_ex is the C = 1 case on the FP32 path.  stride < 1,
+ * pad < 0, N < 1 or a size overflow: CONV_E_SHAPE; CONV_E_LAUNCH if a library
+ * buffer would have to grow while the stream is being captured. */
+B200CONV_API int conv_single_strided_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, int pad,
+                           int stride, float *O, void *stream);
+B200CONV_API int conv_multi_strided_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M,
+                          int pad, int stride, float *O, int precision, void *stream);
+
 /* End-to-end entry points on HOST buffers (pageable or pinned): copy I and F
  * host->device, run the same kernels as the *_ex calls, copy O device->host,
  * and synchronise the stream before returning.  Device scratch comes from a
@@ -176,6 +195,11 @@ B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);
 B200CONV_API int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
 /* Plan of conv_multi_batched_ex (for CONV_FP32 / N == 1: the per-image plan). */
 B200CONV_API int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
+/* Plan of conv_multi_strided_ex (stride > 1: kernel 1 = the per-image KM-SIMT
+ * launch for CONV_FP32, kernel 3 = the one KM-TC/G GEMM over all N images
+ * for CONV_TF32 / CONV_BF16; stride 1: conv_plan_multi_batched of the padded map). */
+B200CONV_API int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride,
+                            int precision, conv_plan *out);
 
 B200CONV_API const char *conv_status_string(int status);
 

@@ -28,7 +28,8 @@ STATUS = {0: "CONV_OK", 1: "CONV_E_SHAPE", 2: "CONV_E_NULL", 3: "CONV_E_ALIGN",
           4: "CONV_E_PRECISION", 5: "CONV_E_DEVICE", 6: "CONV_E_LAUNCH"}
 EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv_single_host",
            "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_multi_batched_ex",
-           "conv_plan_multi_batched", "conv_single_pad_ex", "conv_multi_pad_ex", "conv_plan_single", "conv_plan_multi", "conv_status_string",
+           "conv_plan_multi_batched", "conv_single_pad_ex", "conv_multi_pad_ex",
+           "conv_single_strided_ex", "conv_multi_strided_ex", "conv_plan_multi_strided", "conv_plan_single", "conv_plan_multi", "conv_status_string",
            "conv_version"]
 
 
@@ -75,6 +76,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.conv_single_pad_ex.argtypes = [P, I32, I32, P, I32, I32, I32, P, P]
             lib.conv_multi_pad_ex.argtypes = [P, I32, I32, I32, I32, P, I32, I32, I32, P, I32, P]
             lib.conv_plan_multi_batched.argtypes = [I32, I32, I32, I32, I32, I32, I32, ctypes.POINTER(ConvPlan)]
+            lib.conv_single_strided_ex.argtypes = [P, I32, I32, P, I32, I32, I32, I32, P, P]
+            lib.conv_multi_strided_ex.argtypes = [P, I32, I32, I32, I32, P, I32, I32, I32, I32, P, I32, P]
+            lib.conv_plan_multi_strided.argtypes = [I32, I32, I32, I32, I32, I32, I32, I32, I32,
+                                                    ctypes.POINTER(ConvPlan)]
             lib.conv_status_string.argtypes = [I32]
             lib.conv_status_string.restype = ctypes.c_char_p
             lib.conv_version.argtypes = []
@@ -237,6 +242,44 @@ def multi_batched(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch
     O = out if out is not None else torch.empty((N, M, Wy - K + 1, Wx - K + 1), device=I.device,
                                                 dtype=torch.float32)
     conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision, stream)
+    return O
+
+
+def conv_single_strided_ex(I, Wx, Wy, F, K, M, pad, stride, O, stream=None):
+    _check(load().conv_single_strided_ex(_ptr(I), Wx, Wy, _ptr(F), K, M, pad, stride, _ptr(O), _stream(stream)))
+
+
+def conv_multi_strided_ex(I, N, C, Wx, Wy, F, K, M, pad, stride, O, precision="fp32", stream=None):
+    _check(load().conv_multi_strided_ex(_ptr(I), N, C, Wx, Wy, _ptr(F), K, M, pad, stride, _ptr(O),
+                                        _prec(precision), _stream(stream)))
+
+
+def plan_multi_strided(C, Wx, Wy, K, M, pad, stride, precision="fp32", N=1) -> dict:
+    p = ConvPlan()
+    _check(load().conv_plan_multi_strided(N, C, Wx, Wy, K, M, pad, stride, _prec(precision), ctypes.byref(p)))
+    return p.as_dict()
+
+
+def multi_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0, precision="fp32", stream=None):
+    """Strided, zero-padded Eq. 1: I[N][C][Wy][Wx] -> O[N][M][Ho][Wo],
+    Ho = (Wy+2p-K)//s+1 (= torch.nn.functional.conv2d(I, F, stride=s, padding=p))."""
+    _require_cuda(I, F)
+    N, C, Wy, Wx = I.shape
+    M, _, K, _ = F.shape
+    Ho, Wo = (Wy + 2 * pad - K) // stride + 1, (Wx + 2 * pad - K) // stride + 1
+    O = torch.empty((N, M, Ho, Wo), device=I.device, dtype=torch.float32)
+    conv_multi_strided_ex(I, N, C, Wx, Wy, F, K, M, pad, stride, O, precision, stream)
+    return O
+
+
+def single_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0, stream=None):
+    """Strided, zero-padded Eq. 2 (C = 1, FP32): I[Wy][Wx], F[M][K][K] -> O[M][Ho][Wo]."""
+    _require_cuda(I, F)
+    Wy, Wx = I.shape
+    M, K, _ = F.shape
+    Ho, Wo = (Wy + 2 * pad - K) // stride + 1, (Wx + 2 * pad - K) // stride + 1
+    O = torch.empty((M, Ho, Wo), device=I.device, dtype=torch.float32)
+    conv_single_strided_ex(I, Wx, Wy, F, K, M, pad, stride, O, stream)
     return O
 
 

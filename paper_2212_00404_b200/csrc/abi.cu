@@ -107,6 +107,29 @@ int run_multi(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
     }
 }
 
+// stride sd > 1: FP32 on KM-SIMT, one launch per image;
+// TF32 / BF16 on KM-TC/G (explicit strided im2col of all N images + one TMA GEMM)
+int run_strided(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
+                int precision, int sd, cudaStream_t s) {
+    switch (precision) {
+        case CONV_FP32: {
+            const int64_t out_plane = (int64_t)M * ((Wy - K) / sd + 1) * ((Wx - K) / sd + 1);
+            for (int n = 0; n < N; ++n) {
+                const int st = launch_status(launch_multi_simt(static_cast<const float *>(I) + (size_t)n * C * Wx * Wy,
+                                                               C, Wx, Wy, static_cast<const float *>(F), K, M,
+                                                               O + n * out_plane, s, sd));
+                if (st) return st;
+            }
+            return CONV_OK;
+        }
+        case CONV_TF32:
+        case CONV_BF16:
+            return launch_status(launch_multi_gemm(I, C, Wx, Wy, F, K, M, O, precision == CONV_BF16, s, sd, N));
+        default:
+            return CONV_E_PRECISION;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -370,6 +393,56 @@ int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int prec
     return CONV_OK;
 }
 
+int conv_multi_strided_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad,
+                          int stride, float *O, int precision, void *stream) {
+    if (stride < 1 || pad < 0 || N < 1) return CONV_E_SHAPE;
+    if (stride == 1) return conv_multi_pad_ex(I, N, C, Wx, Wy, F, K, M, pad, O, precision, stream);
+    if (Wx < 1 || Wy < 1 || C < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
+        return CONV_E_SHAPE;
+    const int Wxp = Wx + 2 * pad, Wyp = Wy + 2 * pad;
+    int st = check_shape(C, Wxp, Wyp, K, M);
+    if (st) return st;
+    if ((int64_t)N * C * Wxp * Wyp > INT_MAX) return CONV_E_SHAPE;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    const int e = precision == CONV_BF16 ? 2 : 4;
+    if ((st = check_ptrs(I, F, O, e))) return st;
+    if ((st = check_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const void *Ic = I;
+    if (pad > 0) {
+        void *Ip = padbuf_get((size_t)N * C * Wxp * Wyp * e, s);
+        if (!Ip) return CONV_E_LAUNCH;
+        if ((st = launch_status(launch_pad(I, N * C, Wx, Wy, pad, e, Ip, s)))) return st;
+        Ic = Ip;
+    }
+    if ((int64_t)N * M * ((Wyp - K) / stride + 1) * ((Wxp - K) / stride + 1) > INT_MAX) return CONV_E_SHAPE;
+    return run_strided(Ic, N, C, Wxp, Wyp, F, K, M, O, precision, stride, s);
+}
+
+int conv_single_strided_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, int pad, int stride,
+                           float *O, void *stream) {
+    if (stride == 1) return conv_single_pad_ex(I, Wx, Wy, F, K, M, pad, O, stream);
+    return conv_multi_strided_ex(I, 1, 1, Wx, Wy, F, K, M, pad, stride, O, CONV_FP32, stream);
+}
+
+int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride, int precision,
+                            conv_plan *out) {
+    if (!out) return CONV_E_NULL;
+    if (N < 1 || stride < 1 || pad < 0 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
+        return CONV_E_SHAPE;
+    const int Wxp = Wx + 2 * pad, Wyp = Wy + 2 * pad;
+    if (stride == 1) return conv_plan_multi_batched(N, C, Wxp, Wyp, K, M, precision, out);
+    int st = check_shape(C, Wxp, Wyp, K, M);
+    if (st) return st;
+    switch (precision) {
+        case CONV_FP32: plan_multi_simt(C, Wxp, Wyp, K, M, out, stride); return CONV_OK;
+        case CONV_TF32:
+        case CONV_BF16:
+            return plan_multi_gemm(C, Wxp, Wyp, K, M, precision == CONV_BF16, out, stride, N) ? CONV_E_SHAPE : CONV_OK;
+        default: return CONV_E_PRECISION;
+    }
+}
+
 const char *conv_status_string(int status) {
     switch (status) {
         case CONV_OK: return "ok";
@@ -383,7 +456,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 4; }   // 1.2: + *_host_async; 1.3: + batched; 1.4: + padding
+int conv_version(void) { return (1 << 16) | 5; }   // 1.2: + *_host_async; 1.3: + batched; 1.4: + padding; 1.5: + stride
 
 }  // extern "C"
 

@@ -46,9 +46,15 @@ constexpr int kGmSmemMax = 225 * 1024;
 // ---------------------------------------------------------------- kernel 1
 // X[p][k] for p < P, k < Kp (row stride Kp; zero for k >= C*K*K and outside
 // the channel).  One 16-B vector of consecutive k per thread: coalesced rows.
+// Pixel p = y*Wp + x reads input row y*sd, column x*sd: stride 1 uses wide
+// pixels (Wp = Wx, so the input offset is p itself), stride sd > 1 compact
+// ones (Wp = Wo).
+// Batched (strided calls): pixels p < Ptot = N*Pimg, image n = p / Pimg reads
+// I[n]; rows Ptot <= p < P are zero.
 template <typename T>
 __global__ void __launch_bounds__(256)
-im2col_kernel(const T *__restrict__ I, int C, int Wx, int Wy, int K, int P, int Kp, T *__restrict__ X) {
+im2col_kernel(const T *__restrict__ I, int C, int Wx, int Wy, int K, int P, int Kp, T *__restrict__ X,
+              int sd, int Wp, int Pimg, int Ptot) {
     constexpr int V = 16 / sizeof(T);
     const int KK = K * K, HW = Wx * Wy, Ktot = C * KK;
     const int nv = Kp / V;
@@ -57,18 +63,23 @@ im2col_kernel(const T *__restrict__ I, int C, int Wx, int Wy, int K, int P, int 
     pdl_trigger();
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        const int p = (int)(idx / nv), kv = (int)(idx - (int64_t)p * nv);
+        const int pg = (int)(idx / nv), kv = (int)(idx - (int64_t)pg * nv);
+        const int n = pg / Pimg, p = pg - n * Pimg;          // image, pixel within the image
+        const T *In = I + (int64_t)n * C * HW;
+        const int py = p / Wp;
+        const int base = sd * (py * Wx + (p - py * Wp));   // input offset of the pixel's window
+        const bool live = pg < Ptot;
         int k = kv * V;
         int ch = k / KK, rem = k - ch * KK, r = rem / K, c = rem - r * K;
         union { uint4 u; T e[V]; } v;
 #pragma unroll
         for (int e = 0; e < V; ++e) {
-            const int off = p + r * Wx + c;
-            v.e[e] = (k < Ktot && off < HW) ? I[(int64_t)ch * HW + off] : T(0.f);
+            const int off = base + r * Wx + c;
+            v.e[e] = (live && k < Ktot && off < HW) ? In[(int64_t)ch * HW + off] : T(0.f);
             ++k;
             if (++c == K) { c = 0; if (++r == K) { r = 0; ++ch; } }
         }
-        *reinterpret_cast<uint4 *>(X + (int64_t)p * Kp + (int64_t)kv * V) = v.u;
+        *reinterpret_cast<uint4 *>(X + (int64_t)pg * Kp + (int64_t)kv * V) = v.u;
     }
 }
 
@@ -77,6 +88,7 @@ struct GmArgs {
     int nkb;          // k-blocks of the whole reduction
     int kbps;         // k-blocks per split
     int M, Ho, Wo, Wx;
+    int N;            // images (strided batched calls: compact pixels p = (n*Ho + y)*Wo + x)
     int stages, stage_bytes;
     float *O;
     float *Wk;        // split-K partials [S][tiles][BN][128] (nullptr: DSMEM reduction)
@@ -184,7 +196,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 if constexpr (kModeF) {
                     // row = filter, columns = wide pixels b0 + cb*32 + j
                     const int m = a0 + row;
-                    if (m < g.M) {
+                    if (m < g.M && g.N > 1) {
+                        for (int j = 0; j < 32; ++j) {
+                            const int p = b0 + cb * 32 + j;
+                            int y = p / g.Wx;
+                            const int x = p - y * g.Wx, n = y / g.Ho;
+                            y -= n * g.Ho;
+                            if (n < g.N && x < g.Wo)
+                                g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = __uint_as_float(r[j]);
+                        }
+                    } else if (m < g.M) {
                         const int p = b0 + cb * 32;
                         int y = p / g.Wx, x = p - y * g.Wx;
                         float *orow = g.O + (int64_t)m * plane;
@@ -197,9 +218,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 } else {
                     // row = wide pixel, columns = filters b0 + cb*32 + j
                     const int p = a0 + row;
-                    const int y = p / g.Wx, x = p - y * g.Wx;
-                    if (y < g.Ho && x < g.Wo) {
-                        float *o = g.O + (int64_t)y * g.Wo + x;
+                    int y = p / g.Wx;
+                    const int x = p - y * g.Wx, n = y / g.Ho;      // n = image (0 unless batched)
+                    y -= n * g.Ho;
+                    if (n < g.N && x < g.Wo) {
+                        float *o = g.O + (int64_t)n * g.M * plane + (int64_t)y * g.Wo + x;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int m = b0 + cb * 32 + j;
@@ -259,12 +282,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if constexpr (kModeF) {
                 // column = wide pixel, rows = 4 filters
                 const int p = b0 + nl;
-                const int y = p / g.Wx, x = p - y * g.Wx;
-                if (y < g.Ho && x < g.Wo) {
+                int y = p / g.Wx;
+                const int x = p - y * g.Wx, n = y / g.Ho;
+                y -= n * g.Ho;
+                if (n < g.N && x < g.Wo) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int m = a0 + row0 + e;
-                        if (m < g.M) g.O[(int64_t)m * plane + y * g.Wo + x] = vv[e];
+                        if (m < g.M) g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = vv[e];
                     }
                 }
             } else {
@@ -274,8 +299,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int p = a0 + row0 + e;
-                        const int y = p / g.Wx, x = p - y * g.Wx;
-                        if (y < g.Ho && x < g.Wo) g.O[(int64_t)m * plane + y * g.Wo + x] = vv[e];
+                        int y = p / g.Wx;
+                        const int x = p - y * g.Wx, n = y / g.Ho;
+                        y -= n * g.Ho;
+                        if (n < g.N && x < g.Wo) g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = vv[e];
                     }
                 }
             }
@@ -325,13 +352,17 @@ struct GmPlan {
     size_t x_bytes, w_bytes;
 };
 
-GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16) {
+// sd > 1 (strided calls): compact pixels, and this path is taken whenever it
+// is legal (the implicit kernel is stride-1 only)
+GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N = 1) {
     GmPlan p = {};
     const int elem = bf16 ? 2 : 4, BK = 128 / elem;
-    const int Ho = Wy - K + 1;
+    const int Ho = (Wy - K) / sd + 1;
     const int64_t Ktot = (int64_t)C * K * K;
-    const int64_t Pw = (int64_t)Ho * Wx;                  // wide pixels that carry outputs
-    if ((Ktot * elem) % 16 != 0 || Ktot > (1 << 24) || Pw > (1 << 24)) return p;   // F rows must be TMA-able
+    // (wide) pixels that carry outputs; strided calls: compact, all N images
+    const int64_t Pw = (int64_t)Ho * (sd == 1 ? Wx : (int64_t)N * ((Wx - K) / sd + 1));
+    // F rows must be TMA-able (strided calls re-stride them instead: launch_multi_gemm)
+    if (((Ktot * elem) % 16 != 0 && sd == 1) || Ktot > (1 << 24) || Pw > (1 << 24)) return p;
     p.Kp = (int)((Ktot + BK - 1) / BK * BK);
     p.nkb = p.Kp / BK;
     p.modeF = Pw <= 256;
@@ -354,7 +385,7 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16) {
     // sweep: 24.4 vs 30.2 us bf16).  Pixels-on-M layers stay on the implicit
     // kernel (e.g. 28x28x256: 10.1 vs 16.9 us), B200CONV_GM=2 forces this path.
     const char *force = getenv("B200CONV_GM");
-    if (!(p.modeF && p.tilesA >= 4) && !(force && force[0] == '2')) return p;
+    if (!(p.modeF && p.tilesA >= 4) && !(force && force[0] == '2') && sd == 1) return p;
     const int tiles = p.tilesA * p.tilesB;
     // split the k loop over a cluster: fill the SMs, >= 2 k-blocks per split,
     // and only when the saved k-loop time beats the ~3 us partial exchange
@@ -416,8 +447,8 @@ cudaError_t launch_gemm_bn(const GmPlan &p, const CUtensorMap &ta, const CUtenso
 }
 }  // namespace
 
-int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *out) {
-    const GmPlan p = gm_plan(C, Wx, Wy, K, M, bf16);
+int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *out, int sd, int N) {
+    const GmPlan p = gm_plan(C, Wx, Wy, K, M, bf16, sd, sd > 1 ? N : 1);
     if (!p.ok) return 1;
     out->kernel = 3;
     out->grid_x = p.S;
@@ -436,17 +467,33 @@ int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *o
 // Returns cudaErrorNotSupported when the shape / alignment / workspace does
 // not allow this path (the caller then uses the implicit kernel).
 cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
-                              bool bf16, cudaStream_t s) {
-    const GmPlan p = gm_plan(C, Wx, Wy, K, M, bf16);
-    if (!p.ok || (reinterpret_cast<uintptr_t>(F) % 16) != 0) return cudaErrorNotSupported;
+                              bool bf16, cudaStream_t s, int sd, int N) {
+    if (sd == 1) N = 1;                                     // stride 1: one image (the implicit kernel batches)
+    const GmPlan p = gm_plan(C, Wx, Wy, K, M, bf16, sd, N);
+    if (!p.ok) return cudaErrorNotSupported;
+    const int64_t Ktot0 = (int64_t)C * K * K;
+    // strided calls have no other tensor-core path: filter rows that are not
+    // 16-B strided / aligned are first copied to [M][Kp] with zero tails
+    const bool fpad = ((Ktot0 * (bf16 ? 2 : 4)) % 16 != 0) || (reinterpret_cast<uintptr_t>(F) % 16) != 0;
+    if (fpad && sd == 1) return cudaErrorNotSupported;
     const char *off = getenv("B200CONV_GM");
-    if (off && off[0] == '0') return cudaErrorNotSupported;
+    if (off && off[0] == '0' && sd == 1) return cudaErrorNotSupported;
+    const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
+    const int Wp = sd == 1 ? Wx : Wo;                       // pixel row pitch (wide / compact)
     const int elem = bf16 ? 2 : 4;
     uint8_t *ws = static_cast<uint8_t *>(workspace_get(p.x_bytes + p.w_bytes, s));
     if (!ws) return cudaErrorNotSupported;
     void *X = ws;
     float *Wk = p.S > 1 ? reinterpret_cast<float *>(ws + p.x_bytes) : nullptr;
-    const int64_t Ktot = (int64_t)C * K * K;
+    int64_t Ktot = Ktot0;
+    if (fpad) {
+        void *Fp = auxbuf_get((size_t)M * p.Kp * elem, s);
+        if (!Fp) return cudaErrorNotSupported;
+        cudaError_t e = launch_pad_rows(F, M, (int)Ktot0, p.Kp, elem, Fp, s);
+        if (e != cudaSuccess) return e;
+        F = Fp;
+        Ktot = p.Kp;
+    }
     CUtensorMap tf, tx;
     const int BK = 128 / elem;
     const int frows = p.modeF ? kGmBM : p.BN, xrows = p.modeF ? p.BN : kGmBM;
@@ -469,18 +516,20 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
         cfg.numAttrs = 1;
         cudaError_t e = bf16 ? cudaLaunchKernelEx(&cfg, im2col_kernel<__nv_bfloat16>,
                                                   static_cast<const __nv_bfloat16 *>(I), C, Wx, Wy, K, p.Prows,
-                                                  p.Kp, static_cast<__nv_bfloat16 *>(X))
+                                                  p.Kp, static_cast<__nv_bfloat16 *>(X), sd, Wp, Ho * Wp, N * Ho * Wp)
                              : cudaLaunchKernelEx(&cfg, im2col_kernel<float>, static_cast<const float *>(I), C, Wx,
-                                                  Wy, K, p.Prows, p.Kp, static_cast<float *>(X));
+                                                  Wy, K, p.Prows, p.Kp, static_cast<float *>(X), sd, Wp, Ho * Wp,
+                                                  N * Ho * Wp);
         if (e != cudaSuccess) return e;
     }
     GmArgs g;
     g.nkb = p.nkb;
     g.kbps = p.kbps;
     g.M = M;
-    g.Ho = Wy - K + 1;
-    g.Wo = Wx - K + 1;
-    g.Wx = Wx;
+    g.Ho = Ho;
+    g.Wo = Wo;
+    g.Wx = Wp;
+    g.N = N;
     g.stages = p.stages;
     g.stage_bytes = p.stage_bytes;
     g.O = O;

@@ -58,8 +58,8 @@ int simt_read_stamps(unsigned long long *host) {
 // one thread per output, loads through L1.
 __global__ void __launch_bounds__(256)
 kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F, int K,
-           int M, float *__restrict__ O) {
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+           int M, float *__restrict__ O, int sd) {
+    const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
     const int64_t n = (int64_t)M * Ho * Wo;
     pdl_wait();
     pdl_trigger();
@@ -70,7 +70,7 @@ kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
         const int y = rem / Wo, x = rem - y * Wo;
         float acc = 0.f;
         for (int ch = 0; ch < C; ++ch) {
-            const float *Ic = I + (int64_t)ch * Wx * Wy + (int64_t)y * Wx + x;
+            const float *Ic = I + (int64_t)ch * Wx * Wy + (int64_t)y * sd * Wx + (int64_t)x * sd;
             const float *Fc = F + ((int64_t)m * C + ch) * K * K;
             for (int r = 0; r < K; ++r)
                 for (int c = 0; c < K; ++c) acc = fmaf(__ldg(Ic + (int64_t)r * Wx + c), __ldg(Fc + r * K + c), acc);
@@ -101,7 +101,8 @@ struct SimtShape {
 template <int BM, int BN, int TN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
-           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg) {
+           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg,
+           int sd) {
     using SH = SimtShape<BM, BN, TN>;
     const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const bool tl = dbg && threadIdx.x == 0 && cta_lin < 1024;
@@ -110,7 +111,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     constexpr int TNG = SH::TNG;
     constexpr int T2 = SH::T2;
     const int KK = K * K;
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;   // stride sd (NEXT-3)
     const int HW = Wx * Wy;
     const int HoWo = Ho * Wo;
     const int Ktot = C * KK;
@@ -151,7 +152,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int bo = p0 + bn;
     const bool bvalid = bo < HoWo;
     const int by = bvalid ? bo / Wo : 0;
-    const int bbase = by * Wx + (bvalid ? bo - by * Wo : 0);
+    const int bbase = sd * (by * Wx + (bvalid ? bo - by * Wo : 0));   // input pixel of output (by, bx)
 
     // F rows: thread -> fixed vector column v of rows mr, mr + rpt, ... (chunk
     // invariant, decoded once)
@@ -402,8 +403,8 @@ double sm_time(int n, int q, double w, int nch) {
 
 struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; };
 
-SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd) {
+    const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
     const int64_t px = (int64_t)Ho * Wo;
     const int KK = K * K;
     SimtCfg best = {-1, 1, 1, C, 0, 0, 1e30};
@@ -462,14 +463,16 @@ bool simt_forced(int C, int K, SimtCfg *c) {
     return true;
 }
 
-SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws) {
+SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd) {
     SimtCfg c;
     if (simt_forced(C, K, &c) && (allow_ws || !c.ws)) return c;
-    return simt_choose(C, Wx, Wy, K, M, allow_ws);
+    return simt_choose(C, Wx, Wy, K, M, allow_ws, sd);
 }
 
-void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan *p) {
-    const int64_t px = (int64_t)(Wy - K + 1) * (Wx - K + 1);
+int64_t out_px(int Wx, int Wy, int K, int sd) { return (int64_t)((Wy - K) / sd + 1) * ((Wx - K) / sd + 1); }
+
+void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd) {
+    const int64_t px = out_px(Wx, Wy, K, sd);
     const SimtTile &T = kSimtTiles[c.tile];
     p->kernel = 1;
     p->grid_x = c.S;
@@ -486,10 +489,10 @@ void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan 
 }
 }  // namespace
 
-int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
-    const SimtCfg c = simt_config(C, Wx, Wy, K, M, true);
+int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd) {
+    const SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd);
     if (c.tile < 0) {                                   // naive fallback (huge K)
-        const int64_t n = (int64_t)M * (Wy - K + 1) * (Wx - K + 1);
+        const int64_t n = (int64_t)M * out_px(Wx, Wy, K, sd);
         int64_t blocks = (n + 255) / 256;
         p->kernel = 1;
         p->grid_x = (int)(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
@@ -503,13 +506,13 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p) {
         p->launches = 1;
         return 0;
     }
-    fill_plan(c, C, Wx, Wy, K, M, p);
+    fill_plan(c, C, Wx, Wy, K, M, p, sd);
     return 0;
 }
 
 template <int BM, int BN, int TN>
 static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float *I, int C, int Wx, int Wy,
-                              const float *F, int K, int M, float *O, float *W, cudaStream_t s) {
+                              const float *F, int K, int M, float *O, float *W, cudaStream_t s, int sd) {
     auto kern = kms_kernel<BM, BN, TN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
@@ -534,11 +537,11 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     cfg.numAttrs = W ? 1 : 2;
     const char *dbgs = getenv("B200CONV_SIMT_DBG");
     const int dbg = dbgs ? atoi(dbgs) : 0;
-    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg);
+    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd);
     if (e != cudaSuccess || !W) return e;
     const int ldw = p.grid_y * BN;
     const int64_t slice = (int64_t)p.grid_z * BM * ldw;
-    return launch_splitk_reduce(W, p.grid_x, slice, M, ldw, (Wy - K + 1) * (Wx - K + 1), O, s);
+    return launch_splitk_reduce(W, p.grid_x, slice, M, ldw, (int)out_px(Wx, Wy, K, sd), O, s);
 }
 
 int simt_max_clusters(int cluster, int smem) {
@@ -562,34 +565,34 @@ int simt_max_clusters(int cluster, int smem) {
 }
 
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
-                              float *O, cudaStream_t s) {
-    SimtCfg c = simt_config(C, Wx, Wy, K, M, true);
+                              float *O, cudaStream_t s, int sd) {
+    SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd);
     if (c.tile < 0) {
         conv_plan p;
-        plan_multi_simt(C, Wx, Wy, K, M, &p);
-        kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I, C, Wx, Wy, F, K, M, O);
+        plan_multi_simt(C, Wx, Wy, K, M, &p, sd);
+        kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I, C, Wx, Wy, F, K, M, O, sd);
         return cudaGetLastError();
     }
     float *W = nullptr;
     if (c.ws) {
         const SimtTile &T = kSimtTiles[c.tile];
-        const int64_t px = (int64_t)(Wy - K + 1) * (Wx - K + 1);
+        const int64_t px = out_px(Wx, Wy, K, sd);
         const size_t bytes = (size_t)c.S * ((M + T.BM - 1) / T.BM) * T.BM * ((px + T.BN - 1) / T.BN) * T.BN * 4;
         W = static_cast<float *>(workspace_get(bytes, s));
-        if (!W) c = simt_config(C, Wx, Wy, K, M, false);   // capturing: cluster-only plan
+        if (!W) c = simt_config(C, Wx, Wy, K, M, false, sd);   // capturing: cluster-only plan
     }
     conv_plan p;
-    fill_plan(c, C, Wx, Wy, K, M, &p);
+    fill_plan(c, C, Wx, Wy, K, M, &p, sd);
     switch (c.tile) {
-        case 0: return launch_kms<128, 128, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 1: return launch_kms<64, 256, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 2: return launch_kms<256, 64, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 3: return launch_kms<256, 48, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 4: return launch_kms<128, 96, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 5: return launch_kms<64, 192, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 6: return launch_kms<256, 32, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        case 7: return launch_kms<128, 64, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
-        default: return launch_kms<64, 128, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s);
+        case 0: return launch_kms<128, 128, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 1: return launch_kms<64, 256, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 2: return launch_kms<256, 64, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 3: return launch_kms<256, 48, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 4: return launch_kms<128, 96, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 5: return launch_kms<64, 192, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 6: return launch_kms<256, 32, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 7: return launch_kms<128, 64, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        default: return launch_kms<64, 128, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
     }
 }
 

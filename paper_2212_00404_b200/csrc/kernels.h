@@ -24,10 +24,11 @@ int plan_multi_c3(int C, int Wx, int Wy, int K, int M, conv_plan *p);
 cudaError_t launch_multi_c3(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                             bool bf16, cudaStream_t s);
 
-// KM-SIMT: multi-channel strict FP32 (conv_multi_simt.cu)
-int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p);
+// KM-SIMT: multi-channel strict FP32 (conv_multi_simt.cu); sd = stride
+// (output (Wy-K)/sd+1 x (Wx-K)/sd+1)
+int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd = 1);
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
-                              float *O, cudaStream_t s);
+                              float *O, cudaStream_t s, int sd = 1);
 
 // KM-TC: multi-channel tcgen05 implicit GEMM, TF32 or BF16 (conv_multi_tc.cu)
 // N > 1: a batch of N images, I [N][C][Wy][Wx], O [N][M][Ho][Wo] (shared F)
@@ -38,9 +39,11 @@ cudaError_t launch_multi_tc(const void *I, int C, int Wx, int Wy, const void *F,
 // KM-TC/G: explicit im2col (L2-resident workspace) + TMA-fed tcgen05 GEMM
 // (conv_multi_gemm.cu).  plan returns nonzero / launch returns
 // cudaErrorNotSupported when the shape, alignment or workspace rules it out.
-int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *p);
+// sd > 1: stride (compact pixels; the only tensor-core path for strided calls).
+// N > 1 with sd > 1: all N images (I [N][C][Wy][Wx], O [N][M][Ho][Wo]) in one GEMM.
+int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *p, int sd = 1, int N = 1);
 cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
-                              bool bf16, cudaStream_t s);
+                              bool bf16, cudaStream_t s, int sd = 1, int N = 1);
 
 // Split-K chooser: cluster size S (1..max_split) minimising
 //   waves(S) * (ceil(units / S) * t_unit + (S > 1) * t_reduce),
@@ -58,6 +61,10 @@ int clusters_resident(int S, int ctas_per_sm);
 void *workspace_get(size_t bytes, cudaStream_t s);
 // zero-padded input copies (padded calls): a second per-(device, stream) buffer
 void *padbuf_get(size_t bytes, cudaStream_t s);
+// filter rows re-strided for the strided tensor-core path: a third buffer
+void *auxbuf_get(size_t bytes, cudaStream_t s);
+// Fp[m][k] = F[m][k] (k < Ktot), 0 (Ktot <= k < Kp)
+cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, void *Fp, cudaStream_t s);
 // Ip = I with a zero border of `pad` on every side of each of NC planes
 cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s);
 // O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1

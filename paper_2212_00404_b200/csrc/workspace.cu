@@ -32,6 +32,7 @@ struct WsBuf { void *p = nullptr; size_t bytes = 0; };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_pad;
+std::map<std::pair<int, cudaStream_t>, WsBuf> g_aux;
 std::vector<void *> g_ws_retired;
 }  // namespace
 
@@ -42,6 +43,10 @@ void *workspace_get(size_t bytes, cudaStream_t s) { return buffer_get(g_ws, byte
 // The zero-padded copy of I for padded calls: a second per-(device, stream)
 // buffer, so the kernels of the same call can still use the workspace.
 void *padbuf_get(size_t bytes, cudaStream_t s) { return buffer_get(g_pad, bytes, s); }
+
+// A third per-(device, stream) buffer: filter rows re-strided to a 16-B
+// multiple for the strided tensor-core path (launch_multi_gemm).
+void *auxbuf_get(size_t bytes, cudaStream_t s) { return buffer_get(g_aux, bytes, s); }
 
 static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, size_t bytes, cudaStream_t s) {
     int dev = 0;
@@ -159,6 +164,40 @@ cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem,
                                   Wy, pad, static_cast<__nv_bfloat16 *>(Ip));
     return cudaLaunchKernelEx(&cfg, pad_kernel<float>, static_cast<const float *>(I), NC, Wx, Wy, pad,
                               static_cast<float *>(Ip));
+}
+
+// Fp[m][k] = F[m][k] for k < Ktot, 0 for Ktot <= k < Kp (elem-byte elements)
+template <typename T>
+__global__ void __launch_bounds__(256)
+pad_rows_kernel(const T *__restrict__ F, int M, int Ktot, int Kp, T *__restrict__ Fp) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t total = (int64_t)M * Kp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / Kp;
+        const int k = (int)(i - m * Kp);
+        Fp[i] = k < Ktot ? F[m * Ktot + k] : T(0.f);
+    }
+}
+
+cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, void *Fp, cudaStream_t s) {
+    const int64_t total = (int64_t)M * Kp;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (elem == 2)
+        return cudaLaunchKernelEx(&cfg, pad_rows_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16 *>(F), M,
+                                  Ktot, Kp, static_cast<__nv_bfloat16 *>(Fp));
+    return cudaLaunchKernelEx(&cfg, pad_rows_kernel<float>, static_cast<const float *>(F), M, Ktot, Kp,
+                              static_cast<float *>(Fp));
 }
 
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,

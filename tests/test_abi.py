@@ -22,11 +22,11 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 16
+    assert len(syms) == 19
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16) | 4
+    assert conv.version() == (1 << 16) | 5
 
 
 def test_status_strings():
@@ -148,3 +148,23 @@ def test_padded_argument_errors():
     assert lib.conv_single_pad_ex(f, 8, 8, f, 3, 4, -2, f, None) == 1
     assert lib.conv_single_pad_ex(0, 8, 8, f, 3, 4, 1, f, None) == 2                  # null
     assert lib.conv_multi_pad_ex(f, 1, 2, 8, 8, f, 3, 4, 1, f, 9, None) == 4         # precision
+
+
+def test_strided_argument_errors_and_plans():
+    lib = conv.load()
+    f = 0x1000
+    assert lib.conv_multi_strided_ex(f, 1, 2, 8, 8, f, 3, 4, 0, 0, f, 1, None) == 1      # stride < 1
+    assert lib.conv_multi_strided_ex(f, 1, 2, 8, 8, f, 3, 4, -1, 2, f, 1, None) == 1     # pad < 0
+    assert lib.conv_multi_strided_ex(f, 0, 2, 8, 8, f, 3, 4, 0, 2, f, 1, None) == 1      # N < 1
+    assert lib.conv_multi_strided_ex(f, 1, 2, 2, 2, f, 7, 4, 1, 2, f, 1, None) == 1      # K > padded map
+    assert lib.conv_single_strided_ex(0, 8, 8, f, 3, 4, 0, 2, f, None) == 2               # null
+    assert lib.conv_multi_strided_ex(f, 1, 2, 8, 8, f, 3, 4, 0, 2, f, 9, None) == 4      # precision
+    # stride 1 is the padded / unpadded plan; stride > 1 goes to KM-SIMT (fp32) / KM-TC/G (tf32, bf16)
+    assert conv.plan_multi_strided(64, 28, 28, 3, 64, 1, 1, "tf32") == conv.plan_multi(64, 30, 30, 3, 64, "tf32")
+    for prec, kern in (("fp32", 1), ("tf32", 3), ("bf16", 3)):
+        for (C, W, K, M, pad, s) in [(64, 56, 3, 128, 1, 2), (3, 224, 7, 64, 3, 2), (256, 14, 1, 512, 0, 2)]:
+            p = conv.plan_multi_strided(C, W, W, K, M, pad, s, prec)
+            assert p["kernel"] == kern, (prec, C, W, K, M, pad, s, p)
+            Ho = (W + 2 * pad - K) // s + 1
+            if kern == 1:
+                assert p["grid_y"] * p["tile_n"] >= Ho * Ho        # compact pixel tiles cover the strided map

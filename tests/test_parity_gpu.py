@@ -493,3 +493,61 @@ def test_c3_stem_path_matches_oracle(conv, prec, Wx, Wy, K, M):
     F = synth.uniform_pm1(600 + K, (M, 3, K, K))
     Oo, A = oracle.conv_multi(I, F)
     assert_parity(run_multi(conv, I, F, prec), Oo, A, TAU[prec], f"c3 {Wx}x{Wy} K{K} M{M} {prec}")
+
+
+# ------------------------------------------------------------------ stride > 1
+# O[y][x] = sum I_pad[y*s + r][x*s + c] F[r][c]: the stride-1 valid result of
+# the zero-padded input at rows / columns 0, s, 2s, ... (definition of stride)
+STRIDED = [  # (N, C, Wx, Wy, K, M, pad, stride): ResNet downsampling 3x3/2 and 1x1/2, a 7x7/2 RGB stem,
+    # ragged and odd shapes, unaligned filter rows (C*K*K*elem not a multiple of 16 B), stride 3
+    (1, 64, 56, 56, 3, 128, 1, 2), (1, 256, 14, 14, 1, 512, 0, 2), (1, 3, 33, 29, 7, 20, 3, 2),
+    (2, 20, 17, 11, 3, 70, 0, 3), (1, 7, 9, 12, 5, 33, 2, 2), (3, 16, 28, 28, 3, 40, 1, 2),
+]
+
+
+def _strided_ref(I, F, pad, s):
+    Ip = np.pad(I, ((0, 0), (pad, pad), (pad, pad)))
+    Oo, A = oracle.conv_multi(Ip.astype(np.float32), F)
+    return Oo[:, ::s, ::s], A[:, ::s, ::s]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("N,C,Wx,Wy,K,M,pad,s", STRIDED)
+def test_strided_multi_matches_oracle(conv, prec, N, C, Wx, Wy, K, M, pad, s):
+    I = np.stack([synth.uniform01(70 + n, (C, Wy, Wx)) for n in range(N)])
+    F = synth.uniform_pm1(71, (M, C, K, K))
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    O = conv.multi_strided(torch.from_numpy(I).cuda().to(dt), torch.from_numpy(F).cuda().to(dt), s, pad, prec)
+    torch.cuda.synchronize()
+    Og = O.cpu().numpy().astype(np.float64)
+    for n in range(N):
+        Oo, A = _strided_ref(I[n], F, pad, s)
+        assert_parity(Og[n], Oo, A, TAU[prec], f"strided n={n} {C},{Wx},{Wy},{K},{M},p{pad},s{s} {prec}")
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+def test_strided_integer_inputs_bit_exact(conv, prec):
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    for (C, W, K, M, pad, s) in [(64, 30, 3, 96, 1, 2), (3, 40, 7, 24, 3, 2), (9, 13, 5, 17, 0, 3)]:
+        I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
+        O = conv.multi_strided(torch.from_numpy(I[None]).cuda().to(dt), torch.from_numpy(F).cuda().to(dt), s, pad,
+                               prec)
+        Oo, _ = _strided_ref(I, F, pad, s)
+        assert np.array_equal(O[0].cpu().numpy().astype(np.float64), Oo), (C, W, K, M, pad, s, prec)
+
+
+@pytest.mark.parametrize("Wx,Wy,K,M,pad,s", [(224, 224, 7, 32, 3, 2), (28, 28, 3, 64, 1, 2), (13, 9, 3, 5, 0, 3)])
+def test_strided_single_matches_oracle(conv, Wx, Wy, K, M, pad, s):
+    I = synth.uniform01(72, (Wy, Wx))
+    F = synth.uniform_pm1(73, (M, K, K))
+    O = conv.single_strided(torch.from_numpy(I).cuda(), torch.from_numpy(F).cuda(), s, pad)
+    torch.cuda.synchronize()
+    Oo, A = _strided_ref(I[None], F[:, None], pad, s)
+    assert_parity(O.cpu().numpy().astype(np.float64), Oo, A, TAU["fp32"], f"single strided {Wx},{Wy},{K},{M},p{pad},s{s}")
+
+
+def test_strided_stride1_is_the_padded_call(conv):
+    I = torch.from_numpy(synth.uniform01(74, (2, 16, 20, 20))).cuda()
+    F = torch.from_numpy(synth.uniform_pm1(75, (24, 16, 3, 3))).cuda()
+    for prec in ("fp32", "tf32"):
+        assert torch.equal(conv.multi_strided(I, F, 1, 1, prec), conv.multi_padded(I, F, 1, prec))
