@@ -475,10 +475,12 @@ def _batched(args, conv, dev, stream, pk):
     C, W, K, M = 256, 28, 3, 256
     Ho = W - K + 1
     out = {}
-    for prec in ("tf32", "bf16"):
+    for prec in ("fp32", "tf32", "bf16"):
         dt = torch.bfloat16 if prec == "bf16" else torch.float32
-        peak = pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)
-        for N in (8, 32, 64):
+        # fp32: the strict-FP32 KM-SIMT path, one launch over the batch (frac of the FMA pipe)
+        peak = NUM_SMS * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12 if prec == "fp32" \
+            else pk["bf16_tflops"] * (0.5 if prec == "tf32" else 1.0)
+        for N in ((8, 32) if prec == "fp32" else (8, 32, 64)):
             I = torch.from_numpy(synth.uniform01(synth.SEED_I + N, (N, C, W, W))).to(dev, dt)
             F = torch.from_numpy(synth.uniform_pm1(synth.SEED_F + N, (M, C, K, K))).to(dev, dt)
             Os = [torch.empty((N, M, Ho, Ho), device=dev) for _ in range(3)]
@@ -502,7 +504,7 @@ def _batched(args, conv, dev, stream, pk):
             us = 1e3 * e0.elapsed_time(e1) / reps
             tflops = 2.0 * N * M * C * K * K * Ho * Ho / (us * 1e-6) / 1e12
             out[f"{prec}_n{N}"] = {"us": round(us, 2), "tflops": round(tflops, 1),
-                                   "tensor_frac": round(tflops / peak, 4),
+                                   ("fma_frac" if prec == "fp32" else "tensor_frac"): round(tflops / peak, 4),
                                    "plan": conv.plan_multi_batched(N, C, W, W, K, M, prec)}
     # the same layer as the networks define it: "same" 3x3 convolution (zero
     # padding 1) — pad pre-pass + the batched kernel

@@ -107,21 +107,20 @@ int run_multi(const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
     }
 }
 
-// stride sd > 1: FP32 on KM-SIMT, one launch per image;
-// TF32 / BF16 on KM-TC/G (explicit strided im2col of all N images + one TMA GEMM)
+// the C = 3 stem layers the channel-summing KS variant takes (per image)
+bool c3_layer(int C, int Wx, int Wy, int K, int M) {
+    conv_plan tmp;
+    return plan_multi_c3(C, Wx, Wy, K, M, &tmp) == 0;
+}
+
+// stride sd > 1: FP32 on KM-SIMT, TF32 / BF16 on KM-TC/G
+// (explicit strided im2col + one TMA GEMM); each as ONE launch over all N images
 int run_strided(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                 int precision, int sd, cudaStream_t s) {
     switch (precision) {
-        case CONV_FP32: {
-            const int64_t out_plane = (int64_t)M * ((Wy - K) / sd + 1) * ((Wx - K) / sd + 1);
-            for (int n = 0; n < N; ++n) {
-                const int st = launch_status(launch_multi_simt(static_cast<const float *>(I) + (size_t)n * C * Wx * Wy,
-                                                               C, Wx, Wy, static_cast<const float *>(F), K, M,
-                                                               O + n * out_plane, s, sd));
-                if (st) return st;
-            }
-            return CONV_OK;
-        }
+        case CONV_FP32:
+            return launch_status(launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy,
+                                                   static_cast<const float *>(F), K, M, O, s, sd, N));
         case CONV_TF32:
         case CONV_BF16:
             return launch_status(launch_multi_gemm(I, C, Wx, Wy, F, K, M, O, precision == CONV_BF16, s, sd, N));
@@ -173,8 +172,13 @@ int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const voi
     if ((st = check_ptrs(I, F, O, e))) return st;
     if ((st = check_device())) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (precision == CONV_FP32 && N > 1 && !c3_layer(C, Wx, Wy, K, M)) {
+        // strict FP32: ONE KM-SIMT launch whose pixel tiles span all N images
+        return launch_status(launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy,
+                                               static_cast<const float *>(F), K, M, O, s, 1, N));
+    }
     if (precision == CONV_FP32 || N == 1) {
-        // strict FP32 (and N == 1): one call per image
+        // N == 1, and the C = 3 stem layers (KS-C3): one call per image
         for (int n = 0; n < N; ++n) {
             st = run_multi(static_cast<const uint8_t *>(I) + (size_t)n * C * Wx * Wy * e, C, Wx, Wy, F, K, M,
                            O + (size_t)n * M * Ho * Wo, precision, s);
@@ -387,6 +391,10 @@ int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int prec
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (!out) return CONV_E_NULL;
+    if (precision == CONV_FP32 && N > 1 && !c3_layer(C, Wx, Wy, K, M)) {
+        plan_multi_simt(C, Wx, Wy, K, M, out, 1, N);
+        return CONV_OK;
+    }
     if (precision == CONV_FP32 || N == 1) return conv_plan_multi(C, Wx, Wy, K, M, precision, out);
     if (precision != CONV_TF32 && precision != CONV_BF16) return CONV_E_PRECISION;
     plan_multi_tc(C, Wx, Wy, K, M, precision == CONV_BF16, nullptr, out, N);
@@ -435,7 +443,7 @@ int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad,
     int st = check_shape(C, Wxp, Wyp, K, M);
     if (st) return st;
     switch (precision) {
-        case CONV_FP32: plan_multi_simt(C, Wxp, Wyp, K, M, out, stride); return CONV_OK;
+        case CONV_FP32: plan_multi_simt(C, Wxp, Wyp, K, M, out, stride, N); return CONV_OK;
         case CONV_TF32:
         case CONV_BF16:
             return plan_multi_gemm(C, Wxp, Wyp, K, M, precision == CONV_BF16, out, stride, N) ? CONV_E_SHAPE : CONV_OK;

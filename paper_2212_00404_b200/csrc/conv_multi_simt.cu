@@ -102,7 +102,7 @@ template <int BM, int BN, int TN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
            int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg,
-           int sd) {
+           int sd, int Nimg) {
     using SH = SimtShape<BM, BN, TN>;
     const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const bool tl = dbg && threadIdx.x == 0 && cta_lin < 1024;
@@ -114,6 +114,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;   // stride sd (NEXT-3)
     const int HW = Wx * Wy;
     const int HoWo = Ho * Wo;
+    const int Ptot = Nimg * HoWo;                   // compact pixels of all images (batch)
     const int Ktot = C * KK;
     const int CK = CB * KK;
     const int RS = simt_rs(CK);
@@ -150,9 +151,12 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     constexpr int KL = NT / BN > 0 ? NT / BN : 1;
     const int bn = tid % BN, bkl = tid / BN;
     const int bo = p0 + bn;
-    const bool bvalid = bo < HoWo;
-    const int by = bvalid ? bo / Wo : 0;
-    const int bbase = sd * (by * Wx + (bvalid ? bo - by * Wo : 0));   // input pixel of output (by, bx)
+    const bool bvalid = bo < Ptot;
+    const int bimg = bvalid ? bo / HoWo : 0;
+    const int bpix = bvalid ? bo - bimg * HoWo : 0;
+    const int by = bpix / Wo;
+    // input pixel of output (by, bx) of image bimg
+    const int64_t bbase = (int64_t)bimg * C * HW + sd * (by * Wx + (bpix - by * Wo));
 
     // F rows: thread -> fixed vector column v of rows mr, mr + rpt, ... (chunk
     // invariant, decoded once)
@@ -320,7 +324,7 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int mlo = split * BM / S;                 // rows [mlo, mhi) reduced by this rank
     const int rows = (split + 1) * BM / S - mlo;
     const uint32_t Pbase = smem_u32(P);
-    const int nvalid = min(BN, HoWo - p0);
+    const int nvalid = min(BN, Ptot - p0);
     constexpr int BQ = BN / 4;
     for (int idx = tid; idx < rows * BQ; idx += NT) {
         const int m = mlo + idx / BQ, n = 4 * (idx % BQ);
@@ -331,11 +335,20 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
             v = *reinterpret_cast<const float4 *>(P + m * BN + n);
         }
         if (m0 + m < M) {
-            float *o = O + (int64_t)(m0 + m) * HoWo + p0 + n;   // compact: coalesced
             const float vv[4] = {v.x, v.y, v.z, v.w};
+            if (Nimg == 1) {
+                float *o = O + (int64_t)(m0 + m) * HoWo + p0 + n;   // compact: coalesced
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (n + i < nvalid) o[i] = vv[i];
+                for (int i = 0; i < 4; ++i)
+                    if (n + i < nvalid) o[i] = vv[i];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (n + i >= nvalid) break;
+                    const int q = p0 + n + i, img = q / HoWo;
+                    O[((int64_t)img * M + m0 + m) * HoWo + (q - img * HoWo)] = vv[i];
+                }
+            }
         }
     }
     if (S > 1) cluster_sync_all();
@@ -403,9 +416,9 @@ double sm_time(int n, int q, double w, int nch) {
 
 struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; };
 
-SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd) {
+SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, int Nimg) {
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
-    const int64_t px = (int64_t)Ho * Wo;
+    const int64_t px = (int64_t)Ho * Wo * Nimg;
     const int KK = K * K;
     SimtCfg best = {-1, 1, 1, C, 0, 0, 1e30};
     for (int ti = 0; ti < kNumSimtTiles; ++ti) {
@@ -463,16 +476,16 @@ bool simt_forced(int C, int K, SimtCfg *c) {
     return true;
 }
 
-SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd) {
+SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, int Nimg) {
     SimtCfg c;
     if (simt_forced(C, K, &c) && (allow_ws || !c.ws)) return c;
-    return simt_choose(C, Wx, Wy, K, M, allow_ws, sd);
+    return simt_choose(C, Wx, Wy, K, M, allow_ws, sd, Nimg);
 }
 
 int64_t out_px(int Wx, int Wy, int K, int sd) { return (int64_t)((Wy - K) / sd + 1) * ((Wx - K) / sd + 1); }
 
-void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd) {
-    const int64_t px = out_px(Wx, Wy, K, sd);
+void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd, int Nimg) {
+    const int64_t px = out_px(Wx, Wy, K, sd) * Nimg;
     const SimtTile &T = kSimtTiles[c.tile];
     p->kernel = 1;
     p->grid_x = c.S;
@@ -489,9 +502,9 @@ void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan 
 }
 }  // namespace
 
-int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd) {
-    const SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd);
-    if (c.tile < 0) {                                   // naive fallback (huge K)
+int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd, int Nimg) {
+    const SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd, Nimg);
+    if (c.tile < 0) {                                   // naive fallback (huge K; one image per launch)
         const int64_t n = (int64_t)M * out_px(Wx, Wy, K, sd);
         int64_t blocks = (n + 255) / 256;
         p->kernel = 1;
@@ -506,13 +519,14 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd) {
         p->launches = 1;
         return 0;
     }
-    fill_plan(c, C, Wx, Wy, K, M, p, sd);
+    fill_plan(c, C, Wx, Wy, K, M, p, sd, Nimg);
     return 0;
 }
 
 template <int BM, int BN, int TN>
 static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float *I, int C, int Wx, int Wy,
-                              const float *F, int K, int M, float *O, float *W, cudaStream_t s, int sd) {
+                              const float *F, int K, int M, float *O, float *W, cudaStream_t s, int sd,
+                              int Nimg) {
     auto kern = kms_kernel<BM, BN, TN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
@@ -537,11 +551,12 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     cfg.numAttrs = W ? 1 : 2;
     const char *dbgs = getenv("B200CONV_SIMT_DBG");
     const int dbg = dbgs ? atoi(dbgs) : 0;
-    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd);
+    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd, Nimg);
     if (e != cudaSuccess || !W) return e;
     const int ldw = p.grid_y * BN;
     const int64_t slice = (int64_t)p.grid_z * BM * ldw;
-    return launch_splitk_reduce(W, p.grid_x, slice, M, ldw, (int)out_px(Wx, Wy, K, sd), O, s);
+    const int plane = (int)out_px(Wx, Wy, K, sd);
+    return launch_splitk_reduce(W, p.grid_x, slice, M, ldw, plane * Nimg, O, s, plane);
 }
 
 int simt_max_clusters(int cluster, int smem) {
@@ -565,34 +580,37 @@ int simt_max_clusters(int cluster, int smem) {
 }
 
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
-                              float *O, cudaStream_t s, int sd) {
-    SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd);
+                              float *O, cudaStream_t s, int sd, int Nimg) {
+    SimtCfg c = simt_config(C, Wx, Wy, K, M, true, sd, Nimg);
     if (c.tile < 0) {
         conv_plan p;
         plan_multi_simt(C, Wx, Wy, K, M, &p, sd);
-        kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I, C, Wx, Wy, F, K, M, O, sd);
+        const int64_t out_img = (int64_t)M * out_px(Wx, Wy, K, sd);
+        for (int n = 0; n < Nimg; ++n)
+            kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I + (int64_t)n * C * Wx * Wy, C, Wx, Wy, F, K, M,
+                                                      O + n * out_img, sd);
         return cudaGetLastError();
     }
     float *W = nullptr;
     if (c.ws) {
         const SimtTile &T = kSimtTiles[c.tile];
-        const int64_t px = out_px(Wx, Wy, K, sd);
+        const int64_t px = out_px(Wx, Wy, K, sd) * Nimg;
         const size_t bytes = (size_t)c.S * ((M + T.BM - 1) / T.BM) * T.BM * ((px + T.BN - 1) / T.BN) * T.BN * 4;
         W = static_cast<float *>(workspace_get(bytes, s));
-        if (!W) c = simt_config(C, Wx, Wy, K, M, false, sd);   // capturing: cluster-only plan
+        if (!W) c = simt_config(C, Wx, Wy, K, M, false, sd, Nimg);   // capturing: cluster-only plan
     }
     conv_plan p;
-    fill_plan(c, C, Wx, Wy, K, M, &p, sd);
+    fill_plan(c, C, Wx, Wy, K, M, &p, sd, Nimg);
     switch (c.tile) {
-        case 0: return launch_kms<128, 128, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 1: return launch_kms<64, 256, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 2: return launch_kms<256, 64, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 3: return launch_kms<256, 48, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 4: return launch_kms<128, 96, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 5: return launch_kms<64, 192, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 6: return launch_kms<256, 32, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        case 7: return launch_kms<128, 64, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
-        default: return launch_kms<64, 128, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd);
+        case 0: return launch_kms<128, 128, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 1: return launch_kms<64, 256, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 2: return launch_kms<256, 64, 8>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 3: return launch_kms<256, 48, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 4: return launch_kms<128, 96, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 5: return launch_kms<64, 192, 6>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 6: return launch_kms<256, 32, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        case 7: return launch_kms<128, 64, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
+        default: return launch_kms<64, 128, 4>(c, p, I, C, Wx, Wy, F, K, M, O, W, s, sd, Nimg);
     }
 }
 

@@ -26,9 +26,11 @@ cudaError_t launch_multi_c3(const void *I, int C, int Wx, int Wy, const void *F,
 
 // KM-SIMT: multi-channel strict FP32 (conv_multi_simt.cu); sd = stride
 // (output (Wy-K)/sd+1 x (Wx-K)/sd+1)
-int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd = 1);
+// Nimg > 1: a batch I [Nimg][C][Wy][Wx] -> O [Nimg][M][Ho][Wo] in one launch
+// (pixel tiles over all images' compact pixels)
+int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd = 1, int Nimg = 1);
 cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float *F, int K, int M,
-                              float *O, cudaStream_t s, int sd = 1);
+                              float *O, cudaStream_t s, int sd = 1, int Nimg = 1);
 
 // KM-TC: multi-channel tcgen05 implicit GEMM, TF32 or BF16 (conv_multi_tc.cu)
 // N > 1: a batch of N images, I [N][C][Wy][Wx], O [N][M][Ho][Wo] (shared F)
@@ -67,9 +69,10 @@ void *auxbuf_get(size_t bytes, cudaStream_t s);
 cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, void *Fp, cudaStream_t s);
 // Ip = I with a zero border of `pad` on every side of each of NC planes
 cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s);
-// O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1
+// O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1; plane < N:
+// a batch, column n is pixel n % plane of image n / plane, O [N/plane][M][plane]
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
-                                 cudaStream_t s);
+                                 cudaStream_t s, int plane = 0);
 
 // max co-resident clusters (diagnostics)
 int tc_max_clusters(int cluster, int smem);

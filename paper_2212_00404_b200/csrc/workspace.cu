@@ -81,7 +81,7 @@ static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, siz
 template <int kRedG>
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, int ldw, int N,
-                     float *__restrict__ O) {
+                     float *__restrict__ O, int plane) {
     pdl_wait();
     pdl_trigger();
     // 32-bit indexing: M * N <= INT_MAX is an ABI precondition
@@ -118,11 +118,21 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
             a.w += __shfl_xor_sync(0xffffffffu, a.w, o);
         }
         if (valid && g == 0) {
-            float *o = O + (int64_t)m * N + n;
             const float v[4] = {a.x, a.y, a.z, a.w};
+            if (plane == N) {
+                float *o = O + (int64_t)m * N + n;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (n + i < N) o[i] = v[i];
+                for (int i = 0; i < 4; ++i)
+                    if (n + i < N) o[i] = v[i];
+            } else {
+                // batch of N / plane images: column n + i is pixel (n+i) % plane of image (n+i) / plane
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (n + i >= N) break;
+                    const int img = (n + i) / plane;
+                    O[((int64_t)img * M + m) * plane + (n + i - img * plane)] = v[i];
+                }
+            }
         }
     }
 }
@@ -201,7 +211,8 @@ cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, vo
 }
 
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, int plane) {
+    if (plane <= 0) plane = N;
     // few splits: one lane per float4 of outputs; many: 8 lanes (latency)
     const char *e = getenv("B200CONV_REDG");
     const int G = e ? atoi(e) : (S > 16 ? 8 : 1);
@@ -218,8 +229,8 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8>, W, S, slice, M, ldw, N, O);
-    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1>, W, S, slice, M, ldw, N, O);
+    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8>, W, S, slice, M, ldw, N, O, plane);
+    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1>, W, S, slice, M, ldw, N, O, plane);
 }
 
 }  // namespace b200

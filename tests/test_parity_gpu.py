@@ -551,3 +551,20 @@ def test_strided_stride1_is_the_padded_call(conv):
     F = torch.from_numpy(synth.uniform_pm1(75, (24, 16, 3, 3))).cuda()
     for prec in ("fp32", "tf32"):
         assert torch.equal(conv.multi_strided(I, F, 1, 1, prec), conv.multi_padded(I, F, 1, prec))
+
+
+# strict-FP32 batch in ONE KM-SIMT launch (pixel tiles across images): every
+# thread tile with a cluster and a workspace split, tiles straddling images
+@pytest.mark.parametrize("tile", range(9))
+@pytest.mark.parametrize("split,ws", [(1, 0), (3, 0), (5, 1)])
+def test_simt_batched_every_tile(conv, monkeypatch, tile, split, ws):
+    monkeypatch.setenv("B200CONV_SIMT_FORCE", f"{tile},{split},{ws}")
+    N, C, Wx, Wy, K, M = 3, 20, 17, 11, 3, 70
+    I = np.stack([synth.uniform01(60 + n, (C, Wy, Wx)) for n in range(N)])
+    F = synth.uniform_pm1(61, (M, C, K, K))
+    O = conv.multi_batched(torch.from_numpy(I).cuda(), torch.from_numpy(F).cuda(), "fp32")
+    torch.cuda.synchronize()
+    Og = O.cpu().numpy().astype(np.float64)
+    for n in range(N):
+        Oo, A = oracle.conv_multi(I[n], F)
+        assert_parity(Og[n], Oo, A, TAU["fp32"], f"simt batched tile {tile} split {split} ws {ws} n={n}")
