@@ -110,8 +110,9 @@ B200CONV_API int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void 
  * P:25-42): I [N][C][Wy][Wx], O [N][M][Wy-K+1][Wx-K+1] (device
  * pointers, same element types as conv_multi_ex).  TF32 / BF16: ONE launch of
  * the implicit tensor-core kernel whose pixel tiles span all N images (no
- * split-K needed once N fills the machine).  CONV_FP32 (and N == 1): one
- * conv_multi_ex launch per image.  N < 1 or N*C*Wx*Wy / N*M*Ho*Wo > INT_MAX:
+ * split-K needed once N fills the machine).  CONV_FP32: ONE KM-SIMT launch
+ * whose pixel tiles span all N images (+ the split-K reduce when planned);
+ * the C = 3 stem layers (KS-C3) and N == 1: one conv_multi_ex call per image.  N < 1 or N*C*Wx*Wy / N*M*Ho*Wo > INT_MAX:
  * CONV_E_SHAPE; other errors as conv_multi_ex. */
 B200CONV_API int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M,
                           float *O, int precision, void *stream);
@@ -135,7 +136,7 @@ B200CONV_API int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, 
  * Wo = (Wx+2*pad-K)/stride+1 (torch.nn.functional.conv2d(I, F, stride=stride,
  * padding=pad)).  stride == 1 is exactly conv_*_pad_ex.  stride > 1:
  *   CONV_FP32  KM-SIMT with strided im2col gathers, one launch (+ split-K
- *              reduce) per image;
+ *              reduce) over all N images;
  *   CONV_TF32 / CONV_BF16  KM-TC/G: the strided im2col of all N images into
  *              the workspace, then ONE TMA-fed tcgen05 GEMM; filter rows that are not 16-B
  *              strided are first copied to zero-padded rows in a third
@@ -193,11 +194,12 @@ typedef struct {
 
 B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);
 B200CONV_API int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
-/* Plan of conv_multi_batched_ex (for CONV_FP32 / N == 1: the per-image plan). */
+/* Plan of conv_multi_batched_ex (N == 1 and the C = 3 stem layers in FP32:
+ * the per-image plan). */
 B200CONV_API int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int precision, conv_plan *out);
-/* Plan of conv_multi_strided_ex (stride > 1: kernel 1 = the per-image KM-SIMT
- * launch for CONV_FP32, kernel 3 = the one KM-TC/G GEMM over all N images
- * for CONV_TF32 / CONV_BF16; stride 1: conv_plan_multi_batched of the padded map). */
+/* Plan of conv_multi_strided_ex (stride > 1: kernel 1 = the KM-SIMT launch
+ * for CONV_FP32, kernel 3 = the KM-TC/G GEMM for CONV_TF32 / CONV_BF16, both
+ * over all N images; stride 1: conv_plan_multi_batched of the padded map). */
 B200CONV_API int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride,
                             int precision, conv_plan *out);
 
