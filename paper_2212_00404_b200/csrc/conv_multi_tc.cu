@@ -555,6 +555,211 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     }
 }
 
+// ---------------------------------------------------------------- persistent variant
+// Batched calls with many tiles (S = 1, TMA filters, one 2-D patch box per
+// k-block, C*K*K a multiple of BK): one CTA per SM walks the tiles
+// t = blockIdx.x, + gridDim.x, ...  The rings (stage / parity counters) run
+// on across tiles, so the producers and gather warps start tile t+1 while
+// four dedicated epilogue warps drain tile t's accumulator; the MMA issuer
+// starts tile t+1's MMAs once the epilogue has released TMEM (tmem_empty).
+// This removes the per-tile prologue (TMEM alloc, barrier init, descriptor
+// prefetch) and the pipeline fill that the one-tile-per-CTA kernel pays at
+// every tile.
+constexpr int kTpEpiWarp = 8 + kTcProducers + 1;            // warps 11..14: epilogue
+constexpr int kTpThreads = 32 * (kTpEpiWarp + 4);
+
+template <bool kTF32, int BN>
+__global__ void __launch_bounds__(kTpThreads, 1)
+kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
+                    int C, int Wx, int Wy, int K, int M, float *__restrict__ O, int Nimg, int tiles_y) {
+    using Tr = TcTraits<kTF32>;
+    constexpr int BK = Tr::kBK;
+    constexpr int B_BYTES = BN * 128;
+    constexpr uint32_t IDESC = umma_idesc(Tr::kFmt, kTcBM, BN);
+    const int KK = K * K;
+    const int Ktot = C * KK;
+    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int nkb = Ktot / BK;                           // plan: Ktot % BK == 0
+    const TcGeom geo = tc_geom(Wx, K, BN, Tr::kElem, true);
+    const int NS = geo.stages;
+    const int STAGE = geo.stage_bytes;
+    const int nft = (M + BN - 1) / BN;
+    const int ntiles = tiles_y * nft;                    // tile t: y = t / nft (image x pixel tile), z = t % nft
+    const int npt_img = tiles_y / Nimg;
+    const int64_t plane = (int64_t)Ho * Wo;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint64_t *pfull = full + kTcMaxStages;
+    uint64_t *empty = pfull + kTcMaxStages;
+    uint64_t *tmem_full = empty + kTcMaxStages;          // MMA -> epilogue (one phase per tile)
+    uint64_t *tmem_empty = tmem_full + 1;                // epilogue -> MMA
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 1);
+    int *ktab = reinterpret_cast<int *>(smem + NS * STAGE + 512);
+    for (int idx = threadIdx.x; idx < KK * BK; idx += kTpThreads) {
+        const int u = idx / BK + idx % BK;
+        const int rem = u % KK;
+        ktab[idx] = (u / KK) * geo.npp + (rem / K) * Wx + (rem % K);
+    }
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 8 + 1);                  // 8 gather warps + the filter TMA
+            mbar_init(&pfull[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 4);                        // 4 epilogue warps
+        fence_mbar_init();
+        tma_prefetch_desc(&tmapF);
+        tma_prefetch_desc(&tmapI);
+    }
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
+
+    auto tile_of = [&](int t, int *p0, int *n0, int *img) {
+        const int y = t / nft;
+        *n0 = (t - y * nft) * BN;
+        *img = y / npt_img;
+        *p0 = (y - *img * npt_img) * kTcBM;
+    };
+
+    if (warp >= kProdWarp && warp < kMmaWarp) {
+        // ------------------------------------------------ TMA producers (alternate k-blocks)
+        const int pw = (int)(warp - kProdWarp);
+        if (lane == 0) {
+            int i = 0;                                   // ring iteration across tiles
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int p0, n0, img;
+                tile_of(t, &p0, &n0, &img);
+                int ch_lo = 0;
+                for (int kb = 0; kb < nkb; ++kb, ++i) {
+                    const int k0 = kb * BK;
+                    while ((ch_lo + 1) * KK <= k0) ++ch_lo;
+                    if ((i % kTcProducers) != pw) continue;
+                    const int s = i % NS, ph = (i / NS) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *st = smem + s * STAGE;
+                    mbar_arrive_expect_tx(&pfull[s], (uint32_t)(geo.pch * geo.pb * Tr::kElem));
+                    tma_load_2d(st + B_BYTES, &tmapI, &pfull[s], p0, img * C + ch_lo);
+                    mbar_arrive_expect_tx(&full[s], B_BYTES);
+                    tma_load_2d(st, &tmapF, &full[s], k0, n0);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int i = 0, nt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+                if (nt > 0) {                            // the epilogue has drained the previous tile
+                    mbar_wait(tmem_empty, (uint32_t)((nt - 1) & 1));
+                    tc_fence_after();
+                }
+                for (int kb = 0; kb < nkb; ++kb, ++i) {
+                    const int s = i % NS;
+                    mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+                    tc_fence_after();
+                    const uint32_t b_addr = smem_u32(smem + s * STAGE);
+                    const uint32_t a_tmem = tmem + (uint32_t)(BN + 32 * s);
+#pragma unroll
+                    for (int kk = 0; kk < BK / Tr::kUmmaK; ++kk)
+                        umma_ts<kTF32>(tmem, a_tmem + 8 * kk, umma_desc_k_sw128(b_addr + kk * 32), IDESC,
+                                       (kb > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(tmem_full);                  // this tile's accumulator is complete
+            }
+        }
+        __syncwarp();
+    } else if (warp < 8) {
+        // ------------------------------------------------ im2col build of A (table path)
+        const int gt = threadIdx.x;
+        const int g = gt & 127;
+        const int h = gt >> 7;
+        int i = 0, s = 0, ph = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int ch_lo = 0;
+            for (int kb = 0, k0 = 0; kb < nkb; ++kb, k0 += BK, ++i, (++s == NS) ? (s = 0, ph ^= 1) : 0) {
+                while ((ch_lo + 1) * KK <= k0) ++ch_lo;
+                mbar_wait(&pfull[s], (uint32_t)ph);
+                const uint8_t *patch = smem + s * STAGE + B_BYTES;
+                uint32_t v[16];
+                const int4 *trow = reinterpret_cast<const int4 *>(ktab + (k0 - ch_lo * KK) * BK + (BK / 2) * h);
+                if constexpr (kTF32) {
+                    const float *src = reinterpret_cast<const float *>(patch) + g;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int4 o = trow[q];
+                        v[4 * q] = __float_as_uint(src[o.x]);
+                        v[4 * q + 1] = __float_as_uint(src[o.y]);
+                        v[4 * q + 2] = __float_as_uint(src[o.z]);
+                        v[4 * q + 3] = __float_as_uint(src[o.w]);
+                    }
+                } else {
+                    const unsigned short *src = reinterpret_cast<const unsigned short *>(patch) + g;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int4 o = trow[q];
+                        v[2 * q] = (uint32_t)src[o.x] | ((uint32_t)src[o.y] << 16);
+                        v[2 * q + 1] = (uint32_t)src[o.z] | ((uint32_t)src[o.w] << 16);
+                    }
+                }
+                tmem_st_32x32b_x16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(BN + 32 * s + 16 * h), v);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 11..14)
+        const int q = (int)(warp & 3);                   // TMEM lane quarter
+        const int row = q * 32 + (int)lane;
+        int nt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+            int p0, n0, img;
+            tile_of(t, &p0, &n0, &img);
+            const int pe = p0 + row;
+            const int y = pe / Wx, x = pe - y * Wx;
+            const bool valid = (pe < Ho * Wx) && (x < Wo);
+            float *Oi = O + (int64_t)img * M * plane + (int64_t)y * Wo + x;
+            mbar_wait(tmem_full, (uint32_t)(nt & 1));
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
+                tmem_ld_wait();
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int m = n0 + cb * 32 + j;
+                        if (m < M) Oi[(int64_t)m * plane] = __uint_as_float(r[j]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_empty);      // TMEM free for the next tile's MMAs
+        }
+    }
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -587,7 +792,8 @@ int tc_bn(int M, int pixel_tiles) {
 }
 }  // namespace
 
-int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p, int N) {
+static int plan_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p, int N,
+                   bool allow_persist) {
     const int Ho = Wy - K + 1;
     const int elem = bf16 ? 2 : 4;
     const int BK = 128 / elem;
@@ -625,7 +831,26 @@ int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F,
                          (F == nullptr || (reinterpret_cast<uintptr_t>(F) % 16) == 0);
     p->tma_f = (aligned ? 1 : 0) | (patch ? 2 : 0);    // bit 0: F by TMA, bit 1: I patch by TMA
     p->launches = 1;
+    // persistent variant (kmtc_persist_kernel): more tiles than SMs, no k split,
+    // one 2-D patch box per k-block, whole k-blocks; B200CONV_TC_PERSIST=0 disables
+    const char *pe = getenv("B200CONV_TC_PERSIST");
+    const bool persist_on = allow_persist && !(pe && pe[0] == '0');
+    if (persist_on && S == 1 && aligned && patch && tiles > kNumSMs && gp.nbox == 1 &&
+        ((int64_t)Wx * Wy * elem) % 16 == 0 && Ktot % BK == 0 && gp.tab_bytes > 0) {
+        p->tma_f |= 32;                                    // bit 5: persistent CTAs
+        p->grid_x = 1;
+        p->grid_y = kNumSMs;
+        p->grid_z = 1;
+        p->block_x = kTpThreads;
+    }
     return 0;
+}
+
+int plan_multi_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p, int N) {
+    return plan_tc(C, Wx, Wy, K, M, bf16, F, p, N, true);
+}
+static int plan_tc_nopersist(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F, conv_plan *p, int N) {
+    return plan_tc(C, Wx, Wy, K, M, bf16, F, p, N, false);
 }
 
 template <bool kTF32, int BN, bool kTmaB, bool kPatch>
@@ -668,6 +893,27 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
         Wk = static_cast<float *>(workspace_get(bytes, s));
     }
     return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg, Wk, N);
+}
+
+template <bool kTF32, int BN>
+static cudaError_t launch_tc_persist(const conv_plan &p, const CUtensorMap &tf, const CUtensorMap &ti, int C, int Wx,
+                                     int Wy, int K, int M, float *O, cudaStream_t s, int N) {
+    auto kern = kmtc_persist_kernel<kTF32, BN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    const int tiles_y = N * (((Wy - K + 1) * Wx + kTcBM - 1) / kTcBM);   // images x pixel tiles per image
+    const int tiles = tiles_y * ((M + BN - 1) / BN);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles < kNumSMs ? tiles : kNumSMs);
+    cfg.blockDim = dim3(kTpThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, C, Wx, Wy, K, M, O, N, tiles_y);
 }
 
 template <bool kTF32, int BN>
@@ -722,6 +968,13 @@ static cudaError_t launch_tc_bn(const conv_plan &p, const void *I, int C, int Wx
         }
     }
     conv_plan q = p;
+    if ((p.tma_f & 32) && tma_b && patch && patch2d)
+        return launch_tc_persist<kTF32, BN>(p, tf, ti, C, Wx, Wy, K, M, O, s, N);
+    if (p.tma_f & 32) {                               // planned persistent, but the patch map failed
+        conv_plan r;
+        plan_tc_nopersist(C, Wx, Wy, K, M, !kTF32, F, &r, N);
+        q = r;
+    }
     if (!patch) {
         q.smem_bytes = tc_geom(Wx, K, BN, elem, false).smem;
         return tma_b ? launch_tc<kTF32, BN, true, false>(q, tf, ti, I, C, Wx, Wy, F, K, M, O, patch2d, s, N)

@@ -568,3 +568,25 @@ def test_simt_batched_every_tile(conv, monkeypatch, tile, split, ws):
     for n in range(N):
         Oo, A = oracle.conv_multi(I[n], F)
         assert_parity(Og[n], Oo, A, TAU["fp32"], f"simt batched tile {tile} split {split} ws {ws} n={n}")
+
+
+# persistent KM-TC (more tiles than SMs: each CTA walks several tiles, the
+# epilogue of one overlapping the next one's loads); integer inputs: equal to
+# the one-tile-per-CTA kernel and to the oracle
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_tc_persistent_many_tiles(conv, monkeypatch, prec):
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    N, C, W, K, M = 40, 64, 28, 3, 300                   # 40 x 6 pixel tiles x 2 filter tiles > 148
+    I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
+    Ib = np.stack([np.roll(I, n, axis=-1) for n in range(N)])
+    plan = conv.plan_multi_batched(N, C, W, W, K, M, prec)
+    assert plan["tma_f"] & 32, plan
+    Id, Fd = torch.from_numpy(Ib).cuda().to(dt), torch.from_numpy(F).cuda().to(dt)
+    Op = conv.multi_batched(Id, Fd, prec)
+    monkeypatch.setenv("B200CONV_TC_PERSIST", "0")
+    O1 = conv.multi_batched(Id, Fd, prec)
+    torch.cuda.synchronize()
+    assert torch.equal(Op, O1)
+    for n in (0, 17, N - 1):
+        Oo, _ = oracle.conv_multi(Ib[n], F)
+        assert np.array_equal(Op[n].cpu().numpy().astype(np.float64), Oo), n
