@@ -2,9 +2,10 @@
 // (§2.1 Eq. 1) on the tcgen05 tensor cores with BOTH operands
 // fed by TMA (TF32 or BF16 inputs, FP32 accumulate).
 //
-//   X[p][k] = I[ch][p + r*Wx + c]   (k = (ch, r, c) = ch*K*K + r*K + c,  p = y*Wx + x)
+//   X[p][k] = I[ch][(y*s + r)*Wx + x*s + c]   (k = (ch, r, c) = ch*K*K + r*K + c,
+//                                              p = y*Wo + x compact, stride s)
 //   D       = X . F^T               (F as stored: row-major [M][C*K*K])
-//   O[m][y][x] = D[y*Wx + x][m]     for x < Wo
+//   O[m][y][x] = D[y*Wo + x][m]
 //
 // Why not the implicit kernel (conv_multi_tc.cu) for these layers: there the
 // im2col tile of every k-block is rebuilt by eight warps for every filter
@@ -19,7 +20,7 @@
 // paper, so F is never re-laid out.
 //
 // Two operand roles (chosen per layer by the planner):
-//  * mode P (pixels on the 128-lane M side): A = X tile (128 wide pixels),
+//  * mode P (pixels on the 128-lane M side): A = X tile (128 pixels),
 //    B = F tile (BN filters); many-pixel layers.
 //  * mode F (filters on M): A = F tile (128 filters), B = X tile (all wide
 //    pixels of the map, N <= 256); few-pixel layers (ResNet 14x14 / 7x7, the
@@ -194,7 +195,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
             if (S == 1) {
                 if constexpr (kModeF) {
-                    // row = filter, columns = wide pixels b0 + cb*32 + j
+                    // row = filter, columns = pixels b0 + cb*32 + j
                     const int m = a0 + row;
                     if (m < g.M && g.N > 1) {
                         for (int j = 0; j < 32; ++j) {
@@ -216,7 +217,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         }
                     }
                 } else {
-                    // row = wide pixel, columns = filters b0 + cb*32 + j
+                    // row = pixel, columns = filters b0 + cb*32 + j
                     const int p = a0 + row;
                     int y = p / g.Wx;
                     const int x = p - y * g.Wx, n = y / g.Ho;      // n = image (0 unless batched)
@@ -280,7 +281,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
             const float vv[4] = {v.x, v.y, v.z, v.w};
             if constexpr (kModeF) {
-                // column = wide pixel, rows = 4 filters
+                // column = pixel, rows = 4 filters
                 const int p = b0 + nl;
                 int y = p / g.Wx;
                 const int x = p - y * g.Wx, n = y / g.Ho;
@@ -293,7 +294,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 }
             } else {
-                // column = filter, rows = 4 wide pixels
+                // column = filter, rows = 4 pixels
                 const int m = b0 + nl;
                 if (m < g.M) {
 #pragma unroll
@@ -344,7 +345,11 @@ bool encode_2d(CUtensorMap *m, bool tf32, const void *base, uint64_t inner, uint
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int round_bn(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 192 ? 192 : 256)); }
+// pixel-side tile width (mode F: N of the MMA): the smallest instantiated
+// width >= n (every X byte a CTA streams is TMA ingest, ~53 B/clk per SM)
+int round_bn(int n) {
+    return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 160 ? 160 : (n <= 192 ? 192 : 256))));
+}
 
 struct GmPlan {
     bool ok, modeF;
@@ -360,7 +365,9 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N
     const int Ho = (Wy - K) / sd + 1;
     const int64_t Ktot = (int64_t)C * K * K;
     // (wide) pixels that carry outputs; strided calls: compact, all N images
-    const int64_t Pw = (int64_t)Ho * (sd == 1 ? Wx : (int64_t)N * ((Wx - K) / sd + 1));
+    // compact output pixels (p = (n*Ho + y)*Wo + x) of all N images: no wide
+    // columns x >= Wo in the X operand (the sweep: 144 instead of 168 rows)
+    const int64_t Pw = (int64_t)Ho * N * ((Wx - K) / sd + 1);
     // F rows must be TMA-able (strided calls re-stride them instead: launch_multi_gemm)
     if (((Ktot * elem) % 16 != 0 && sd == 1) || Ktot > (1 << 24) || Pw > (1 << 24)) return p;
     p.Kp = (int)((Ktot + BK - 1) / BK * BK);
@@ -439,7 +446,9 @@ template <bool kTF32, bool kModeF>
 cudaError_t launch_gemm_bn(const GmPlan &p, const CUtensorMap &ta, const CUtensorMap &tb, const GmArgs &g,
                            cudaStream_t s) {
     switch (p.BN) {
+        case 32: return launch_gemm<kTF32, 32, kModeF>(p, ta, tb, g, s);
         case 64: return launch_gemm<kTF32, 64, kModeF>(p, ta, tb, g, s);
+        case 160: return launch_gemm<kTF32, 160, kModeF>(p, ta, tb, g, s);
         case 128: return launch_gemm<kTF32, 128, kModeF>(p, ta, tb, g, s);
         case 192: return launch_gemm<kTF32, 192, kModeF>(p, ta, tb, g, s);
         default: return launch_gemm<kTF32, 256, kModeF>(p, ta, tb, g, s);
@@ -457,7 +466,7 @@ int plan_multi_gemm(int C, int Wx, int Wy, int K, int M, bool bf16, conv_plan *o
     out->block_x = kGmThreads;
     out->cluster_x = p.S;
     out->tile_m = p.modeF ? kGmBM : p.BN;               // filters per tile
-    out->tile_n = p.modeF ? p.BN : kGmBM;               // wide pixels per tile
+    out->tile_n = p.modeF ? p.BN : kGmBM;               // pixels per tile
     out->smem_bytes = p.smem;
     out->tma_f = 1 | 4 | (p.modeF ? 8 : 0);             // F by TMA, X (im2col) by TMA, filters-on-M
     out->launches = 2;
@@ -479,7 +488,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     const char *off = getenv("B200CONV_GM");
     if (off && off[0] == '0' && sd == 1) return cudaErrorNotSupported;
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
-    const int Wp = sd == 1 ? Wx : Wo;                       // pixel row pitch (wide / compact)
+    const int Wp = Wo;                                      // compact pixel rows
     const int elem = bf16 ? 2 : 4;
     uint8_t *ws = static_cast<uint8_t *>(workspace_get(p.x_bytes + p.w_bytes, s));
     if (!ws) return cudaErrorNotSupported;
