@@ -183,12 +183,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_wait(tmem_full, 0);
             tc_fence_after();
         }
+        constexpr int NCB = (BN + 31) / 32;           // 32-column blocks; BN % 32 == 16: a 16-column tail
 #pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {
+        for (int cb = 0; cb < NCB; ++cb) {
             uint32_t r[32];
-            if (niter > 0) {
+            const int ncol = (BN % 32 != 0 && cb == NCB - 1) ? BN % 32 : 32;
+            if (niter > 0 && ncol == 32) {
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
                 tmem_ld_wait();
+            } else if (niter > 0) {
+                tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 16; j < 32; ++j) r[j] = 0u;
             } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) r[j] = 0u;
@@ -198,7 +205,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     // row = filter, columns = pixels b0 + cb*32 + j
                     const int m = a0 + row;
                     if (m < g.M && g.N > 1) {
-                        for (int j = 0; j < 32; ++j) {
+                        for (int j = 0; j < ncol; ++j) {
                             const int p = b0 + cb * 32 + j;
                             int y = p / g.Wx;
                             const int x = p - y * g.Wx, n = y / g.Ho;
@@ -233,7 +240,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) P[(cb * 32 + j) * kGmBM + row] = __uint_as_float(r[j]);
+                for (int j = 0; j < 32; ++j)
+                    if (j < ncol) P[(cb * 32 + j) * kGmBM + row] = __uint_as_float(r[j]);
             }
         }
         if (S > 1 && g.Wk) fence_proxy_async_smem();    // P -> visible to the bulk store
@@ -348,7 +356,7 @@ bool encode_2d(CUtensorMap *m, bool tf32, const void *base, uint64_t inner, uint
 // pixel-side tile width (mode F: N of the MMA): the smallest instantiated
 // width >= n (every X byte a CTA streams is TMA ingest, ~53 B/clk per SM)
 int round_bn(int n) {
-    return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 160 ? 160 : (n <= 192 ? 192 : 256))));
+    return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 144 ? 144 : (n <= 160 ? 160 : (n <= 192 ? 192 : 256)))));
 }
 
 struct GmPlan {
@@ -448,6 +456,7 @@ cudaError_t launch_gemm_bn(const GmPlan &p, const CUtensorMap &ta, const CUtenso
     switch (p.BN) {
         case 32: return launch_gemm<kTF32, 32, kModeF>(p, ta, tb, g, s);
         case 64: return launch_gemm<kTF32, 64, kModeF>(p, ta, tb, g, s);
+        case 144: return launch_gemm<kTF32, 144, kModeF>(p, ta, tb, g, s);
         case 160: return launch_gemm<kTF32, 160, kModeF>(p, ta, tb, g, s);
         case 128: return launch_gemm<kTF32, 128, kModeF>(p, ta, tb, g, s);
         case 192: return launch_gemm<kTF32, 192, kModeF>(p, ta, tb, g, s);
