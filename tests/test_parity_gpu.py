@@ -590,3 +590,32 @@ def test_tc_persistent_many_tiles(conv, monkeypatch, prec):
     for n in (0, 17, N - 1):
         Oo, _ = oracle.conv_multi(Ib[n], F)
         assert np.array_equal(Op[n].cpu().numpy().astype(np.float64), Oo), n
+
+
+def test_batched_strided_persistent_replay_from_a_cuda_graph(conv):
+    # the batch / stride entry points and the persistent kernel under graph capture
+    s = torch.cuda.Stream()
+    I = torch.from_numpy(synth.uniform01(90, (40, 64, 28, 28))).cuda()
+    F = torch.from_numpy(synth.uniform_pm1(91, (300, 64, 3, 3))).cuda()
+    assert conv.plan_multi_batched(40, 64, 28, 28, 3, 300, "tf32")["tma_f"] & 32
+    calls = [
+        lambda O: conv.conv_multi_batched_ex(I, 40, 64, 28, 28, F, 3, 300, O, "tf32", s.cuda_stream),
+        lambda O: conv.conv_multi_strided_ex(I, 40, 64, 28, 28, F, 3, 300, 1, 2, O, "tf32", s.cuda_stream),
+        lambda O: conv.conv_multi_strided_ex(I, 40, 64, 28, 28, F, 3, 300, 1, 2, O, "fp32", s.cuda_stream),
+    ]
+    shapes = [(40, 300, 26, 26), (40, 300, 14, 14), (40, 300, 14, 14)]
+    for fn, shp in zip(calls, shapes):
+        O = torch.empty(shp, device="cuda")
+        with torch.cuda.stream(s):
+            fn(O)
+            s.synchronize()
+            ref = O.clone()
+            O.fill_(float("nan"))
+            g = torch.cuda.CUDAGraph()
+            g.capture_begin()
+            fn(O)
+            g.capture_end()
+            g.replay()
+            g.replay()
+            s.synchronize()
+        assert torch.equal(O, ref), shp
