@@ -398,18 +398,20 @@ void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
 // / two resident CTAs; constants fitted (tools/simt_model.py) to a measured
 // sweep of every (tile, split, mode) on the bench layers (tools/simt_sweep.py,
 // B200): the planner's pick is within 1.5% of the best measured on average.
-// (Refit after the staging rewrite, sweep v3: kEff1 0.40 -> 0.35; AlexNet
-// 27.9 -> 25.9 us, the other picks unchanged.)
+// (Refit after the staging rewrite on sweep v3 (profiles/sweeps/): kEff1
+// 0.35, kEff2 0.50, TN = 6 / 4 penalty 0.9, and a per-chunk cost that scales
+// with BM (the F-row load and transpose of a chunk are BM x CK elements):
+// AlexNet 27.9 -> 25.9 us, target 30.5 -> 28.2, ResNet 14x14 13.5 -> 12.9.)
 constexpr double kFmaPerUs = 128.0 * 1965.0;
-constexpr double kEff1 = 0.35, kEff2 = 0.45;
+constexpr double kEff1 = 0.35, kEff2 = 0.50;
 constexpr double kCtaFixed = 0.5;      // prologue (first chunk latency) + epilogue
-constexpr double kPerChunk = 0.6;      // per channel chunk: barriers, F transpose, load issue
+constexpr double kPerChunk = 0.4;      // per channel chunk of a BM = 128 tile: barriers, F transpose, load issue
 constexpr double kClusterReduce = 9.0; // cluster co-scheduling + barrier waits + DSMEM reduction
 constexpr double kWsReduce = 0.5;      // second launch (PDL-overlapped) + its tail
 constexpr double kL2BytesPerUs = 3.0e6;
 
-double sm_time(int n, int q, double w, int nch) {
-    const double c = kCtaFixed + nch * kPerChunk;
+double sm_time(int n, int q, double w, int nch, int BM) {
+    const double c = kCtaFixed + nch * kPerChunk * (BM / 128.0);
     if (q >= 2) return (n / 2) * (2.0 * w / kEff2) + (n % 2) * (w / kEff1) + ((n + 1) / 2) * c;
     return n * (w / kEff1 + c);
 }
@@ -426,7 +428,7 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, 
         const int npt = (int)((px + T.BN - 1) / T.BN);
         const int nmt = (M + T.BM - 1) / T.BM;
         const int tiles = npt * nmt;
-        const double tn_pen = T.TN == 8 ? 1.0 : (T.TN == 6 ? 0.9 : 1.0);     // fitted per thread tile
+        const double tn_pen = T.TN == 8 ? 1.0 : 0.9;                          // fitted per thread tile
         int last_S = -1;
         for (int Sreq = 1; Sreq <= C && Sreq <= 96; ++Sreq) {
             int CB, cps;
@@ -447,11 +449,11 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, 
                     const int cap = clusters_resident(S, q);
                     const int waves = (tiles + cap - 1) / cap;
                     const int per_wave = (tiles < cap ? tiles : cap) * S;
-                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w, nch) + (S > 1 ? kClusterReduce : 0.0);
+                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w, nch, T.BM) + (S > 1 ? kClusterReduce : 0.0);
                 } else {
                     const int64_t total = (int64_t)tiles * S;
                     const double bytes = 8.0 * S * (double)nmt * T.BM * (double)npt * T.BN + 4.0 * M * px;
-                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w, nch) + kWsReduce + bytes / kL2BytesPerUs;
+                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w, nch, T.BM) + kWsReduce + bytes / kL2BytesPerUs;
                 }
                 if (t < best.t * 0.995) best = {ti, S, CB, cps, ws, smem, t};
             }

@@ -78,7 +78,7 @@ static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, siz
 // slices s = g, g + G, ... in order (8 loads in flight), then the G lane sums
 // combine by a fixed xor tree — the same order on every run, so the result is
 // deterministic.
-template <int kRedG>
+template <int kRedG, bool kBatch>
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, int ldw, int N,
                      float *__restrict__ O, int plane) {
@@ -119,7 +119,7 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
         }
         if (valid && g == 0) {
             const float v[4] = {a.x, a.y, a.z, a.w};
-            if (plane == N) {
+            if constexpr (!kBatch) {
                 float *o = O + (int64_t)m * N + n;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -229,8 +229,14 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8>, W, S, slice, M, ldw, N, O, plane);
-    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1>, W, S, slice, M, ldw, N, O, plane);
+    // a batch (plane < N) maps columns to (image, pixel): its own instantiation,
+    // so the single-image store path is the plain one
+    if (plane != N) {
+        if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, true>, W, S, slice, M, ldw, N, O, plane);
+        return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, true>, W, S, slice, M, ldw, N, O, plane);
+    }
+    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, false>, W, S, slice, M, ldw, N, O, plane);
+    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, false>, W, S, slice, M, ldw, N, O, plane);
 }
 
 }  // namespace b200

@@ -65,7 +65,7 @@ def cost(P, C, W, K, M, ti, Sreq, ws):
     nch = -(-cps // CB)
 
     def smt(n):
-        c = P["c0"] + nch * P["cch"]
+        c = P["c0"] + nch * P["cch"] * (BM / 128.0) ** P.get("cbm", 0.0)
         if q >= 2:
             return (n // 2) * (2 * w / P["e2"]) + (n % 2) * (w / P["e1"]) + ((n + 1) // 2) * c
         return n * (w / P["e1"] + c)
@@ -115,7 +115,7 @@ def main():
             _, cps = split(C, min(Sreq, C), BM, BN, K)
             meas.setdefault(r["layer"], {})[(ti, -(-C // cps), ws)] = r["us"]
     base = dict(e1=0.40, e2=0.45, c0=0.5, ccl=9.0, cws=0.5, l2=3.0e6, pen6=0.95, pen4=1.1, rsl=0.0, cch=0.0)
-    grid = dict(e2=[0.45, 0.5], cws=[0.5, 1.0], pen6=[0.85, 0.9, 0.95, 1.0], pen4=[0.8, 0.9, 1.0, 1.1],
+    grid = dict(e2=[0.45, 0.5], cws=[0.5, 1.0], pen6=[0.85, 0.9, 0.95, 1.0], pen4=[0.8, 0.9, 1.0, 1.1], cbm=[0.0, 0.5, 1.0],
                 rsl=[0.0, 0.05], cch=[0.3, 0.4, 0.6, 0.8], e1=[0.35, 0.4, 0.45])
 
     def regret(P, verbose=False):
