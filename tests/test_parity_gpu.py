@@ -574,9 +574,10 @@ def test_simt_batched_every_tile(conv, monkeypatch, tile, split, ws):
 # epilogue of one overlapping the next one's loads); integer inputs: equal to
 # the one-tile-per-CTA kernel and to the oracle
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
-def test_tc_persistent_many_tiles(conv, monkeypatch, prec):
+@pytest.mark.parametrize("M", [300, 200, 64])          # filter tiles of 256 (ragged), 128 (ragged), 64
+def test_tc_persistent_many_tiles(conv, monkeypatch, prec, M):
     dt = torch.bfloat16 if prec == "bf16" else torch.float32
-    N, C, W, K, M = 40, 64, 28, 3, 300                   # 40 x 6 pixel tiles x 2 filter tiles > 148
+    N, C, W, K = 40, 64, 28, 3                           # 40 x 6 pixel tiles (x filter tiles) > 148
     I, F = synth.layer_inputs(C, W, W, K, M, kind="ints")
     Ib = np.stack([np.roll(I, n, axis=-1) for n in range(N)])
     plan = conv.plan_multi_batched(N, C, W, W, K, M, prec)
