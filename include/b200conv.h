@@ -187,7 +187,8 @@ typedef struct {
     int tile_n;        /* (wide) output pixels per CTA tile */
     int smem_bytes;    /* dynamic shared memory per CTA */
     int tma_f;         /* bit 0: F tiles by TMA; bit 1: I patch by TMA (KM-TC); bit 2: im2col tiles by
-                          TMA (KM-TC/G); bit 3: filters on the 128-lane M side (KM-TC/G) */
+                          TMA (KM-TC/G); bit 3: filters on the 128-lane M side (KM-TC/G); bit 5:
+                          persistent KM-TC (grid_y CTAs, one per SM, walk all tiles; block_x 480) */
     int launches;      /* kernel launches per call: 1, or 2 (split-K through the workspace;
                           cluster_x is then 1 and grid_x is the split count) */
 } conv_plan;
