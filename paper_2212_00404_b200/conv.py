@@ -83,6 +83,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             lib.conv_status_string.argtypes = [I32]
             lib.conv_status_string.restype = ctypes.c_char_p
             lib.conv_version.argtypes = []
+            lib.conv_diag_nop.argtypes = [P]
+            lib.conv_diag_nop.restype = I32
             for n in EXPORTS:
                 if n != "conv_status_string":
                     getattr(lib, n).restype = I32
@@ -183,6 +185,11 @@ def plan_multi(C, Wx, Wy, K, M, precision="fp32") -> dict:
     p = ConvPlan()
     _check(load().conv_plan_multi(C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
     return p.as_dict()
+
+
+def diag_nop(stream=None):
+    """One empty kernel with the hot path's launch attributes (launch floor)."""
+    _check(load().conv_diag_nop(_stream(stream)))
 
 
 def version() -> int:

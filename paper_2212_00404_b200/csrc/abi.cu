@@ -470,6 +470,9 @@ int conv_version(void) { return (1 << 16) | 5; }   // 1.2: + *_host_async; 1.3: 
 
 // ------------------------------------------------------------ diagnostics
 // Max co-resident clusters for a kernel family at a cluster size (tools only).
+extern "C" B200CONV_API int conv_diag_nop(void *stream) {
+    return launch_status(launch_nop(static_cast<cudaStream_t>(stream)));
+}
 extern "C" B200CONV_API int conv_diag_stamps(unsigned long long *host) { return tc_read_stamps(host); }
 extern "C" B200CONV_API int conv_diag_ks_stamps(unsigned long long *host) { return ks_read_stamps(host); }
 extern "C" B200CONV_API int conv_diag_ks_fine(unsigned long long *host) { return ks_read_fine(host); }

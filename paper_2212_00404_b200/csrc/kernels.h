@@ -74,6 +74,9 @@ cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem,
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
                                  cudaStream_t s, int plane = 0);
 
+// empty PDL-attributed kernel (the launch floor, diagnostics)
+cudaError_t launch_nop(cudaStream_t s);
+
 // max co-resident clusters (diagnostics)
 int tc_max_clusters(int cluster, int smem);
 int tc_read_stamps(unsigned long long *host);

@@ -239,4 +239,24 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
     return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, false>, W, S, slice, M, ldw, N, O, plane);
 }
 
+// empty kernel with the same launch attributes as the hot-path kernels: the
+// dependent-launch floor every call of the library pays (bench launch_floor_us)
+__global__ void nop_kernel() {
+    pdl_wait();
+    pdl_trigger();
+}
+
+cudaError_t launch_nop(cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, nop_kernel);
+}
+
 }  // namespace b200
