@@ -27,21 +27,42 @@
  * pointer owned by the caller; the library keeps no pointer after the call.
  * The library allocates (i) its workspace — split-K partial tiles and the
  * KM-TC/G im2col matrix — and (ii) the zero-padded input copy of the padded
- * calls: one device buffer each per (device, stream), grown on demand outside
- * stream capture (geometric growth; superseded buffers stay allocated, since
- * a graph captured earlier may still reference them) and kept for the process
- * lifetime.  During stream capture a call never allocates: a shape whose
- * workspace would have to grow takes a plan that needs none (cluster / DSMEM
- * reduction, implicit tensor-core kernel); a padded call returns
- * CONV_E_LAUNCH.  The *_host entry points take host pointers and use a
- * library-owned stream-ordered memory pool.  O must not overlap I or F.
+ * calls: one device buffer each per (device, stream), grown on demand
+ * (geometric growth; superseded buffers stay allocated, since work in flight
+ * may still reference them) and kept for the process lifetime.  A call made
+ * while its stream is being captured into a CUDA graph does not use those
+ * shared buffers: its scratch is a graph memory allocation (cudaMallocAsync
+ * node before its kernels, cudaFreeAsync node after them) private to the
+ * captured graph, so graphs captured on one stream may be replayed
+ * concurrently on different streams.  Two threads issuing calls on the SAME
+ * stream handle (e.g. cudaStreamPerThread is one value for all threads, or
+ * the legacy stream) share that stream's buffers: such calls must be ordered
+ * by the stream itself, as any work on one stream is.  The *_host entry
+ * points take host pointers and use a library-owned stream-ordered memory
+ * pool.  O must not overlap I or F.
  *
  * Execution: asynchronous and stream-ordered on the given stream (a
  * cudaStream_t / CUstream passed as void*; NULL = legacy default stream);
  * no host synchronisation inside the device entry points.  Kernel faults
- * surface at the caller's next synchronisation.  Reentrant: no mutable global
- * state except one-time kernel attribute setup and the workspace cache
- * (mutex-protected).
+ * surface at the caller's next synchronisation.  Reentrant: the only mutable
+ * global state is the per-kernel shared-memory limit (raised monotonically
+ * under a mutex, never lowered), the per-device SM-count / cluster-occupancy
+ * cache and the workspace cache (mutex-protected).
+ *
+ * Planner overrides (environment, read at each call; they only choose among
+ * correct plans, the tests force every path with them, unset = the planner):
+ *   B200CONV_PDL=0          no programmatic dependent launch
+ *   B200CONV_GM=0|2         KM-TC/G im2col+GEMM path off | forced where legal
+ *   B200CONV_GM_SPLIT=S     KM-TC/G k split (cluster size) S
+ *   B200CONV_TC_BN=32..256  KM-TC filter-tile width
+ *   B200CONV_TC_SPLIT=S     KM-TC k split S
+ *   B200CONV_TC_PERSIST=0   no persistent KM-TC for batched calls
+ *   B200CONV_TC_DSMEM=1     KM-TC split-K partials reduced through DSMEM
+ *   B200CONV_SIMT_FORCE=t,S,ws  KM-SIMT thread tile t, channel split S, ws=1:
+ *                           reduced through the workspace
+ *   B200CONV_C3=0           no KS-C3 (C = 3 stems take the general kernels)
+ * Timeline stamps and work-skipping diagnostics exist only in the separate
+ * -DB200CONV_DIAG build (libb200conv_diag.so), never in this library.
  *
  * Errors: the return value is a conv_status.  On any argument error nothing is
  * launched and O is untouched.  Checks, in order:
@@ -172,8 +193,9 @@ B200CONV_API int conv_single_host_async(const float *I, int Wx, int Wy, const fl
 B200CONV_API int conv_multi_host_async(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                           int precision, void *stream);
 
-/* Launch plan the device entry points use for a shape (pure function; no
- * device access).  A call of the hot path is one kernel launch, or two when
+/* Launch plan the device entry points use for a shape (a function of the
+ * shape and of the current device's SM count / cluster occupancy, queried
+ * once; B200 values when no device is present; no device memory access).  A call of the hot path is one kernel launch, or two when
  * the channel split is reduced through the library's split-K workspace
  * (launches == 2: a deterministic fixed-order reduction kernel follows). */
 typedef struct {

@@ -197,19 +197,58 @@ def version() -> int:
 
 
 # ---------------------------------------------------------------- conveniences
-def _require_cuda(*ts):
-    for t in ts:
-        if not (t.is_cuda and t.is_contiguous()):
-            raise ValueError("expected contiguous CUDA tensors")
+# Every convenience validates its tensors before any pointer reaches the ABI:
+# the C entry points only see raw pointers and sizes, so a wrong dtype, shape,
+# device or stride here would become an out-of-bounds access there.
+def _want_dtype(precision):
+    return torch.bfloat16 if _prec(precision) == CONV_BF16 else torch.float32
+
+
+def _check_inputs(I, F, precision, i_dims, f_dims, cuda=True):
+    where = "CUDA" if cuda else "CPU"
+    want = _want_dtype(precision)
+    for name, t, nd in (("I", I, i_dims), ("F", F, f_dims)):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor")
+        if t.is_cuda != cuda:
+            raise ValueError(f"{name} must be a {where} tensor")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if t.dim() != nd:
+            raise ValueError(f"{name} must have {nd} dimensions, got shape {tuple(t.shape)}")
+        if t.dtype != want:
+            raise ValueError(f"precision {precision} expects {want} {name}, got {t.dtype}")
+    if cuda and I.device != F.device:
+        raise ValueError("I and F must be on the same device")
+    if F.shape[-1] != F.shape[-2]:
+        raise ValueError(f"F must hold square K x K filters, got {tuple(F.shape)}")
+    if f_dims == 4 and F.shape[1] != I.shape[-3]:
+        raise ValueError(f"channel mismatch: I has {I.shape[-3]} channels, F {F.shape[1]}")
+
+
+def _output(out, shape, like, cuda=True):
+    if out is None:
+        return torch.empty(shape, device=like.device if cuda else "cpu", dtype=torch.float32)
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out must be a float32 tensor of shape {tuple(shape)}")
+    if out.is_cuda != cuda or (cuda and out.device != like.device) or not out.is_contiguous():
+        raise ValueError("out must be contiguous and on the inputs' device")
+    return out
+
+
+def _out_hw(Wy, Wx, K, pad=0, stride=1):
+    Ho, Wo = (Wy + 2 * pad - K) // stride + 1, (Wx + 2 * pad - K) // stride + 1
+    if K < 1 or Ho < 1 or Wo < 1 or pad < 0 or stride < 1:
+        raise ValueError(f"K={K} does not fit the {Wy}x{Wx} map (pad {pad}, stride {stride})")
+    return Ho, Wo
 
 
 def single(I: torch.Tensor, F: torch.Tensor, out: torch.Tensor | None = None, stream=None):
     """Eq. 2: I[Wy][Wx] f32, F[M][K][K] f32 -> O[M][Ho][Wo] f32 (kernel KS)."""
-    _require_cuda(I, F)
+    _check_inputs(I, F, "fp32", 2, 3)
     Wy, Wx = I.shape
     M, K, _ = F.shape
-    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), device=I.device,
-                                                dtype=torch.float32)
+    O = _output(out, (M, *_out_hw(Wy, Wx, K)), I)
     conv_single_ex(I, Wx, Wy, F, K, M, O, stream)
     return O
 
@@ -220,16 +259,10 @@ def multi(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor 
 
     precision "fp32" (KM-SIMT), "tf32" (KM-TC) take float32 I, F; "bf16"
     (KM-TC) takes bfloat16 I, F."""
-    _require_cuda(I, F)
-    want = torch.bfloat16 if _prec(precision) == CONV_BF16 else torch.float32
-    if I.dtype != want or F.dtype != want:
-        raise ValueError(f"precision {precision} expects {want} inputs")
+    _check_inputs(I, F, precision, 3, 4)
     C, Wy, Wx = I.shape
-    M, C2, K, _ = F.shape
-    if C2 != C:
-        raise ValueError("channel mismatch")
-    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), device=I.device,
-                                                dtype=torch.float32)
+    M, _, K, _ = F.shape
+    O = _output(out, (M, *_out_hw(Wy, Wx, K)), I)
     conv_multi_ex(I, C, Wx, Wy, F, K, M, O, precision, stream)
     return O
 
@@ -238,16 +271,10 @@ def multi_batched(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch
                   stream=None):
     """Eq. 1 on a batch: I[N][C][Wy][Wx], F[M][C][K][K] -> O[N][M][Ho][Wo] f32
     (= torch.nn.functional.conv2d(I, F) without padding, stride 1)."""
-    _require_cuda(I, F)
-    want = torch.bfloat16 if _prec(precision) == CONV_BF16 else torch.float32
-    if I.dtype != want or F.dtype != want:
-        raise ValueError(f"precision {precision} expects {want} inputs")
+    _check_inputs(I, F, precision, 4, 4)
     N, C, Wy, Wx = I.shape
-    M, C2, K, _ = F.shape
-    if C2 != C:
-        raise ValueError("channel mismatch")
-    O = out if out is not None else torch.empty((N, M, Wy - K + 1, Wx - K + 1), device=I.device,
-                                                dtype=torch.float32)
+    M, _, K, _ = F.shape
+    O = _output(out, (N, M, *_out_hw(Wy, Wx, K)), I)
     conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision, stream)
     return O
 
@@ -267,46 +294,47 @@ def plan_multi_strided(C, Wx, Wy, K, M, pad, stride, precision="fp32", N=1) -> d
     return p.as_dict()
 
 
-def multi_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0, precision="fp32", stream=None):
+def multi_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0, precision="fp32",
+                  out: torch.Tensor | None = None, stream=None):
     """Strided, zero-padded Eq. 1: I[N][C][Wy][Wx] -> O[N][M][Ho][Wo],
     Ho = (Wy+2p-K)//s+1 (= torch.nn.functional.conv2d(I, F, stride=s, padding=p))."""
-    _require_cuda(I, F)
+    _check_inputs(I, F, precision, 4, 4)
     N, C, Wy, Wx = I.shape
     M, _, K, _ = F.shape
-    Ho, Wo = (Wy + 2 * pad - K) // stride + 1, (Wx + 2 * pad - K) // stride + 1
-    O = torch.empty((N, M, Ho, Wo), device=I.device, dtype=torch.float32)
+    O = _output(out, (N, M, *_out_hw(Wy, Wx, K, pad, stride)), I)
     conv_multi_strided_ex(I, N, C, Wx, Wy, F, K, M, pad, stride, O, precision, stream)
     return O
 
 
-def single_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0, stream=None):
+def single_strided(I: torch.Tensor, F: torch.Tensor, stride: int, pad: int = 0,
+                   out: torch.Tensor | None = None, stream=None):
     """Strided, zero-padded Eq. 2 (C = 1, FP32): I[Wy][Wx], F[M][K][K] -> O[M][Ho][Wo]."""
-    _require_cuda(I, F)
+    _check_inputs(I, F, "fp32", 2, 3)
     Wy, Wx = I.shape
     M, K, _ = F.shape
-    Ho, Wo = (Wy + 2 * pad - K) // stride + 1, (Wx + 2 * pad - K) // stride + 1
-    O = torch.empty((M, Ho, Wo), device=I.device, dtype=torch.float32)
+    O = _output(out, (M, *_out_hw(Wy, Wx, K, pad, stride)), I)
     conv_single_strided_ex(I, Wx, Wy, F, K, M, pad, stride, O, stream)
     return O
 
 
-def multi_padded(I: torch.Tensor, F: torch.Tensor, pad: int, precision="fp32", stream=None):
+def multi_padded(I: torch.Tensor, F: torch.Tensor, pad: int, precision="fp32", out: torch.Tensor | None = None,
+                 stream=None):
     """Zero-padded Eq. 1: I[N][C][Wy][Wx] -> O[N][M][Wy+2p-K+1][Wx+2p-K+1]
     (= torch.nn.functional.conv2d(I, F, padding=pad))."""
-    _require_cuda(I, F)
+    _check_inputs(I, F, precision, 4, 4)
     N, C, Wy, Wx = I.shape
     M, _, K, _ = F.shape
-    O = torch.empty((N, M, Wy + 2 * pad - K + 1, Wx + 2 * pad - K + 1), device=I.device, dtype=torch.float32)
+    O = _output(out, (N, M, *_out_hw(Wy, Wx, K, pad)), I)
     conv_multi_pad_ex(I, N, C, Wx, Wy, F, K, M, pad, O, precision, stream)
     return O
 
 
-def single_padded(I: torch.Tensor, F: torch.Tensor, pad: int, stream=None):
+def single_padded(I: torch.Tensor, F: torch.Tensor, pad: int, out: torch.Tensor | None = None, stream=None):
     """Zero-padded Eq. 2: I[Wy][Wx], F[M][K][K] -> O[M][Wy+2p-K+1][Wx+2p-K+1]."""
-    _require_cuda(I, F)
+    _check_inputs(I, F, "fp32", 2, 3)
     Wy, Wx = I.shape
     M, K, _ = F.shape
-    O = torch.empty((M, Wy + 2 * pad - K + 1, Wx + 2 * pad - K + 1), device=I.device, dtype=torch.float32)
+    O = _output(out, (M, *_out_hw(Wy, Wx, K, pad)), I)
     conv_single_pad_ex(I, Wx, Wy, F, K, M, pad, O, stream)
     return O
 
@@ -314,16 +342,19 @@ def single_padded(I: torch.Tensor, F: torch.Tensor, pad: int, stream=None):
 def multi_host(I: torch.Tensor, F: torch.Tensor, precision="fp32", out: torch.Tensor | None = None,
                stream=None):
     """End-to-end on host tensors through conv_multi_host (H2D, kernel, D2H, sync)."""
+    _check_inputs(I, F, precision, 3, 4, cuda=False)
     C, Wy, Wx = I.shape
     M, _, K, _ = F.shape
-    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), dtype=torch.float32)
+    O = _output(out, (M, *_out_hw(Wy, Wx, K)), I, cuda=False)
     conv_multi_host(I, C, Wx, Wy, F, K, M, O, precision, stream)
     return O
 
 
 def single_host(I: torch.Tensor, F: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """End-to-end on host tensors through conv_single_host (H2D, kernel, D2H, sync)."""
+    _check_inputs(I, F, "fp32", 2, 3, cuda=False)
     Wy, Wx = I.shape
     M, K, _ = F.shape
-    O = out if out is not None else torch.empty((M, Wy - K + 1, Wx - K + 1), dtype=torch.float32)
+    O = _output(out, (M, *_out_hw(Wy, Wx, K)), I, cuda=False)
     conv_single_host(I, Wx, Wy, F, K, M, O, stream)
     return O

@@ -2,28 +2,115 @@
 // device check, dispatch to one kernel launch per call, host-buffer entry
 // points.  Every compute step of the hot path runs in the kernels; this file
 // only checks and launches.
+#include <array>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 #include "kernels.h"
 
 using namespace b200;
 
-int b200::pdl_enabled() {
-    const char *e = getenv("B200CONV_PDL");
-    return (e && e[0] == '0') ? 0 : 1;
+int b200::pdl_enabled() { return env_override("B200CONV_PDL", 1) != 0; }
+
+int b200::env_override(const char *name, int def) {
+    const char *e = getenv(name);
+    if (!e || !*e) return def;
+    char *end = nullptr;
+    const long v = strtol(e, &end, 10);
+    return end == e ? def : (int)v;
 }
 
-// co-resident clusters of size S on a B200 (148 SMs, 8 GPCs), measured with
-// cudaOccupancyMaxActiveClusters for our kernels (tools/cluster_occ.py)
+static int current_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
+    return dev;
+}
+
+int b200::num_sms() {
+    static std::atomic<int> cache[64];
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        return 148;
+    }
+    cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
+cudaError_t b200::ensure_smem(const void *kernel, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, int> limit;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    int &cur = limit[{dev, kernel}];
+    if (bytes <= cur) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
+
+// Co-resident clusters of size S for kernels that fit 1 or 2 CTAs per SM:
+// cudaOccupancyMaxActiveClusters of a probe kernel with the same residency
+// (256 threads, 200 KB or 100 KB of shared memory), queried once per device.
+// Without a device (host-only plan queries) the values measured on B200 are
+// used (148 SMs, 8 GPCs; tools/cluster_occ.py).
 static const int kClusters1[17] = {0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7};
 static const int kClusters2[17] = {0, 296, 148, 93, 71, 56, 45, 37, 33, 30, 26, 21, 21, 17, 14, 14, 14};
 
+__global__ void occ_probe_kernel() {}
+
+static const int *cluster_table(int ctas_per_sm) {
+    static std::mutex mu;
+    static std::map<int, std::array<int, 34>> tabs;
+    const int dev = current_device();
+    const int which = ctas_per_sm >= 2 ? 1 : 0;
+    if (dev < 0) return which ? kClusters2 : kClusters1;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = tabs.find(dev);
+    if (it == tabs.end()) {
+        std::array<int, 34> t{};
+        bool ok = true;
+        for (int w = 0; w < 2 && ok; ++w) {
+            const int smem = w ? 100 * 1024 : 200 * 1024;
+            ok = ensure_smem((const void *)occ_probe_kernel, smem) == cudaSuccess;
+            for (int S = 1; S <= 16 && ok; ++S) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(S);
+                cfg.blockDim = dim3(256);
+                cfg.dynamicSmemBytes = smem;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = S;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int n = 0;
+                ok = cudaOccupancyMaxActiveClusters(&n, occ_probe_kernel, &cfg) == cudaSuccess && n > 0;
+                t[17 * w + S] = n;
+            }
+        }
+        if (!ok) {
+            cudaGetLastError();
+            for (int S = 0; S < 17; ++S) { t[S] = kClusters1[S]; t[17 + S] = kClusters2[S]; }
+        }
+        it = tabs.emplace(dev, t).first;
+    }
+    return it->second.data() + 17 * which;
+}
+
 int b200::choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_unit,
                        float t_reduce) {
-    const int *tab = ctas_per_sm >= 2 ? kClusters2 : kClusters1;
+    const int *tab = cluster_table(ctas_per_sm);
     if (max_split > 16) max_split = 16;
     if (max_split > units) max_split = units;
     int best = 1;
@@ -40,7 +127,7 @@ int b200::choose_split(int tiles, int units, int max_split, int ctas_per_sm, flo
 int b200::clusters_resident(int S, int ctas_per_sm) {
     if (S < 1) S = 1;
     if (S > 16) S = 16;
-    return (ctas_per_sm >= 2 ? kClusters2 : kClusters1)[S];
+    return cluster_table(ctas_per_sm)[S];
 }
 
 namespace {
@@ -135,6 +222,7 @@ extern "C" {
 
 int conv_single_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                    void *stream) {
+    CallScope scope;
     int st = check_shape(1, Wx, Wy, K, M);
     if (st) return st;
     if ((st = check_ptrs(I, F, O, 4))) return st;
@@ -148,6 +236,7 @@ int conv_single(const float *I, int Wx, int Wy, const float *F, int K, int M, fl
 
 int conv_multi_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                   int precision, void *stream) {
+    CallScope scope;
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
@@ -162,6 +251,7 @@ int conv_multi(const float *I, int C, int Wx, int Wy, const float *F, int K, int
 
 int conv_multi_batched_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                           int precision, void *stream) {
+    CallScope scope;
     if (N < 1) return CONV_E_SHAPE;
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
@@ -266,6 +356,7 @@ static int single_body(const void *I, const void *F, float *O, void *c) {
 
 int conv_single_host(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                      void *stream) {
+    CallScope scope;
     int st = check_shape(1, Wx, Wy, K, M);
     if (st) return st;
     if ((st = check_ptrs(I, F, O, 4))) return st;
@@ -278,6 +369,7 @@ int conv_single_host(const float *I, int Wx, int Wy, const float *F, int K, int 
 
 int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                     int precision, void *stream) {
+    CallScope scope;
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
@@ -293,6 +385,7 @@ int conv_multi_host(const void *I, int C, int Wx, int Wy, const void *F, int K, 
 // Asynchronous variants: identical, minus the final stream synchronisation.
 int conv_single_host_async(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                            void *stream) {
+    CallScope scope;
     int st = check_shape(1, Wx, Wy, K, M);
     if (st) return st;
     if ((st = check_ptrs(I, F, O, 4))) return st;
@@ -305,6 +398,7 @@ int conv_single_host_async(const float *I, int Wx, int Wy, const float *F, int K
 
 int conv_multi_host_async(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, float *O,
                           int precision, void *stream) {
+    CallScope scope;
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
@@ -337,8 +431,7 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
         case CONV_TF32:
         case CONV_BF16: {
             const bool bf16 = precision == CONV_BF16;
-            const char *gm = getenv("B200CONV_GM");
-            if ((gm && gm[0] == '0') || plan_multi_gemm(C, Wx, Wy, K, M, bf16, out) != 0)
+            if (env_override("B200CONV_GM", 1) == 0 || plan_multi_gemm(C, Wx, Wy, K, M, bf16, out) != 0)
                 plan_multi_tc(C, Wx, Wy, K, M, bf16, nullptr, out);
             return CONV_OK;
         }
@@ -349,6 +442,7 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
 // ------------------------------------------------------------ zero padding
 int conv_single_pad_ex(const float *I, int Wx, int Wy, const float *F, int K, int M, int pad, float *O,
                        void *stream) {
+    CallScope scope;
     if (pad < 0) return CONV_E_SHAPE;
     if (pad == 0) return conv_single_ex(I, Wx, Wy, F, K, M, O, stream);
     if (Wx < 1 || Wy < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
@@ -367,6 +461,7 @@ int conv_single_pad_ex(const float *I, int Wx, int Wy, const float *F, int K, in
 
 int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad, float *O,
                       int precision, void *stream) {
+    CallScope scope;
     if (pad < 0 || N < 1) return CONV_E_SHAPE;
     if (pad == 0) return conv_multi_batched_ex(I, N, C, Wx, Wy, F, K, M, O, precision, stream);
     if (Wx < 1 || Wy < 1 || C < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
@@ -403,6 +498,7 @@ int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int prec
 
 int conv_multi_strided_ex(const void *I, int N, int C, int Wx, int Wy, const void *F, int K, int M, int pad,
                           int stride, float *O, int precision, void *stream) {
+    CallScope scope;
     if (stride < 1 || pad < 0 || N < 1) return CONV_E_SHAPE;
     if (stride == 1) return conv_multi_pad_ex(I, N, C, Wx, Wy, F, K, M, pad, O, precision, stream);
     if (Wx < 1 || Wy < 1 || C < 1 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
@@ -411,6 +507,7 @@ int conv_multi_strided_ex(const void *I, int N, int C, int Wx, int Wy, const voi
     int st = check_shape(C, Wxp, Wyp, K, M);
     if (st) return st;
     if ((int64_t)N * C * Wxp * Wyp > INT_MAX) return CONV_E_SHAPE;
+    if ((int64_t)N * M * ((Wyp - K) / stride + 1) * ((Wxp - K) / stride + 1) > INT_MAX) return CONV_E_SHAPE;
     if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
     const int e = precision == CONV_BF16 ? 2 : 4;
     if ((st = check_ptrs(I, F, O, e))) return st;
@@ -423,7 +520,6 @@ int conv_multi_strided_ex(const void *I, int N, int C, int Wx, int Wy, const voi
         if ((st = launch_status(launch_pad(I, N * C, Wx, Wy, pad, e, Ip, s)))) return st;
         Ic = Ip;
     }
-    if ((int64_t)N * M * ((Wyp - K) / stride + 1) * ((Wxp - K) / stride + 1) > INT_MAX) return CONV_E_SHAPE;
     return run_strided(Ic, N, C, Wxp, Wyp, F, K, M, O, precision, stride, s);
 }
 
@@ -464,7 +560,7 @@ const char *conv_status_string(int status) {
     }
 }
 
-int conv_version(void) { return (1 << 16) | 5; }   // 1.2: + *_host_async; 1.3: + batched; 1.4: + padding; 1.5: + stride
+int conv_version(void) { return (1 << 16) | 6; }   // 1.2: + *_host_async; 1.3: + batched; 1.4: + padding; 1.5: + stride; 1.6: graph-private scratch
 
 }  // extern "C"
 

@@ -399,17 +399,16 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N
     // with >= 4 filter tiles (ResNet 7x7: 8.4 vs 11.8 us bf16; configs[4]
     // sweep: 24.4 vs 30.2 us bf16).  Pixels-on-M layers stay on the implicit
     // kernel (e.g. 28x28x256: 10.1 vs 16.9 us), B200CONV_GM=2 forces this path.
-    const char *force = getenv("B200CONV_GM");
-    if (!(p.modeF && p.tilesA >= 4) && !(force && force[0] == '2') && sd == 1) return p;
+    if (!(p.modeF && p.tilesA >= 4) && env_override("B200CONV_GM", 1) != 2 && sd == 1) return p;
     const int tiles = p.tilesA * p.tilesB;
     // split the k loop over a cluster: fill the SMs, >= 2 k-blocks per split,
     // and only when the saved k-loop time beats the ~3 us partial exchange
-    int S = tiles >= kNumSMs ? 1 : kNumSMs / tiles;
+    int S = tiles >= num_sms() ? 1 : num_sms() / tiles;
     if (S > kGmMaxSplit) S = kGmMaxSplit;
     if (S > p.nkb / 2) S = p.nkb / 2 > 0 ? p.nkb / 2 : 1;
     while (S > 1 && tiles > clusters_resident(S, 1)) --S;
     if (S > 1 && p.nkb <= 8) S = 1;
-    if (const char *e = getenv("B200CONV_GM_SPLIT")) { const int v = atoi(e); if (v >= 1 && v <= kGmMaxSplit) S = v; }
+    if (const int v = env_override("B200CONV_GM_SPLIT", 0); v >= 1 && v <= kGmMaxSplit) S = v;
     p.kbps = (p.nkb + S - 1) / S;
     p.S = (p.nkb + p.kbps - 1) / p.kbps;
     p.stage_bytes = kGmBM * 128 + p.BN * 128;
@@ -427,12 +426,8 @@ template <bool kTF32, int BN, bool kModeF>
 cudaError_t launch_gemm(const GmPlan &p, const CUtensorMap &ta, const CUtensorMap &tb, const GmArgs &g,
                         cudaStream_t s) {
     auto kern = gemm_kernel<kTF32, BN, kModeF>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+    cudaError_t e = ensure_smem((const void *)kern, p.smem);
     if (e != cudaSuccess) return e;
-    if (p.S > 8) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.S, p.tilesA, p.tilesB);
     cfg.blockDim = dim3(kGmThreads);
@@ -494,8 +489,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     // 16-B strided / aligned are first copied to [M][Kp] with zero tails
     const bool fpad = ((Ktot0 * (bf16 ? 2 : 4)) % 16 != 0) || (reinterpret_cast<uintptr_t>(F) % 16) != 0;
     if (fpad && sd == 1) return cudaErrorNotSupported;
-    const char *off = getenv("B200CONV_GM");
-    if (off && off[0] == '0' && sd == 1) return cudaErrorNotSupported;
+    if (env_override("B200CONV_GM", 1) == 0 && sd == 1) return cudaErrorNotSupported;
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
     const int Wp = Wo;                                      // compact pixel rows
     const int elem = bf16 ? 2 : 4;
@@ -522,7 +516,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     {
         const int64_t vecs = (int64_t)p.Prows * (p.Kp / (16 / elem));
         int blocks = (int)((vecs + 255) / 256);
-        if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+        if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(blocks);
         cfg.blockDim = dim3(256);

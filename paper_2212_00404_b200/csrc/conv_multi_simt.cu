@@ -101,9 +101,10 @@ struct SimtShape {
 template <int BM, int BN, int TN>
 __global__ void __launch_bounds__(kSimtThreads, 2)
 kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
-           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg,
+           int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg_in,
            int sd, int Nimg) {
     using SH = SimtShape<BM, BN, TN>;
+    const int dbg = kDiag ? dbg_in : 0;
     const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const bool tl = dbg && threadIdx.x == 0 && cta_lin < 1024;
     if (tl) g_simt_cta[5 * cta_lin] = simt_gtimer();
@@ -449,11 +450,11 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, 
                     const int cap = clusters_resident(S, q);
                     const int waves = (tiles + cap - 1) / cap;
                     const int per_wave = (tiles < cap ? tiles : cap) * S;
-                    t = waves * sm_time((per_wave + kNumSMs - 1) / kNumSMs, q, w, nch, T.BM) + (S > 1 ? kClusterReduce : 0.0);
+                    t = waves * sm_time((per_wave + num_sms() - 1) / num_sms(), q, w, nch, T.BM) + (S > 1 ? kClusterReduce : 0.0);
                 } else {
                     const int64_t total = (int64_t)tiles * S;
                     const double bytes = 8.0 * S * (double)nmt * T.BM * (double)npt * T.BN + 4.0 * M * px;
-                    t = sm_time((int)((total + kNumSMs - 1) / kNumSMs), q, w, nch, T.BM) + kWsReduce + bytes / kL2BytesPerUs;
+                    t = sm_time((int)((total + num_sms() - 1) / num_sms()), q, w, nch, T.BM) + kWsReduce + bytes / kL2BytesPerUs;
                 }
                 if (t < best.t * 0.995) best = {ti, S, CB, cps, ws, smem, t};
             }
@@ -510,7 +511,7 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd, i
         const int64_t n = (int64_t)M * out_px(Wx, Wy, K, sd);
         int64_t blocks = (n + 255) / 256;
         p->kernel = 1;
-        p->grid_x = (int)(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
+        p->grid_x = (int)(blocks < 4 * num_sms() ? blocks : 4 * num_sms());
         p->grid_y = p->grid_z = 1;
         p->block_x = 256;
         p->cluster_x = 1;
@@ -530,13 +531,8 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
                               const float *F, int K, int M, float *O, float *W, cudaStream_t s, int sd,
                               int Nimg) {
     auto kern = kms_kernel<BM, BN, TN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         p.smem_bytes);
+    cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
-    if (p.cluster_x > 8) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid_x, p.grid_y, p.grid_z);
     cfg.blockDim = dim3(p.block_x);
@@ -551,8 +547,7 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = W ? 1 : 2;
-    const char *dbgs = getenv("B200CONV_SIMT_DBG");
-    const int dbg = dbgs ? atoi(dbgs) : 0;
+    const int dbg = kDiag ? env_override("B200CONV_SIMT_DBG", 0) : 0;
     e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd, Nimg);
     if (e != cudaSuccess || !W) return e;
     const int ldw = p.grid_y * BN;
@@ -563,8 +558,7 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
 
 int simt_max_clusters(int cluster, int smem) {
     auto kern = kms_kernel<128, 128, 8>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_smem((const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster, 1, 1);
     cfg.blockDim = dim3(kSimtThreads);

@@ -136,8 +136,9 @@ template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 __global__ void __launch_bounds__(kTcThreads, 1)
 kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
             const void *__restrict__ Iv, const void *__restrict__ Fv, int C, int Wx, int Wy,
-            int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg,
+            int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg_in,
             float *__restrict__ Wk, int Nimg) {
+    const int dbg = kDiag ? dbg_in : 0;
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
     constexpr int BK = Tr::kBK;
@@ -781,10 +782,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // per 256 filters: batched 28x28x256, N = 32: 105 vs 125 us TF32, 64 vs 84 us
 // BF16; single images keep N = 128 tiles and split k instead.)
 int tc_bn(int M, int pixel_tiles) {
-    if (const char *e = getenv("B200CONV_TC_BN")) {        // experiments: 32 / 64 / 128 / 256
-        const int v = atoi(e);
-        if (v == 32 || v == 64 || v == 128 || v == 256) return v;
-    }
+    if (const int v = env_override("B200CONV_TC_BN", 0); v == 32 || v == 64 || v == 128 || v == 256) return v;
     if (M <= 32) return 32;
     if (M <= 64) return 64;
     if (M >= 1024 || (M >= 256 && pixel_tiles >= 64)) return 256;
@@ -810,10 +808,7 @@ static int plan_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F
     int S = tiles >= 128 ? 1
                          : choose_split(tiles, nkb, nkb / 2 < kTcMaxSplit ? (nkb / 2 > 0 ? nkb / 2 : 1) : kTcMaxSplit,
                                         1, 0.45f, 3.5f);
-    if (const char *e = getenv("B200CONV_TC_SPLIT")) {     // experiments
-        const int v = atoi(e);
-        if (v >= 1 && v <= kTcMaxSplit && v <= nkb) S = v;
-    }
+    if (const int v = env_override("B200CONV_TC_SPLIT", 0); v >= 1 && v <= kTcMaxSplit && v <= nkb) S = v;
     const TcGeom gp = tc_geom(Wx, K, BN, elem, true);
     const bool patch = gp.stages >= 2;
     const TcGeom g = patch ? gp : tc_geom(Wx, K, BN, elem, false);
@@ -833,13 +828,12 @@ static int plan_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F
     p->launches = 1;
     // persistent variant (kmtc_persist_kernel): more tiles than SMs, no k split,
     // one 2-D patch box per k-block, whole k-blocks; B200CONV_TC_PERSIST=0 disables
-    const char *pe = getenv("B200CONV_TC_PERSIST");
-    const bool persist_on = allow_persist && !(pe && pe[0] == '0');
-    if (persist_on && S == 1 && aligned && patch && tiles > kNumSMs && gp.nbox == 1 &&
+    const bool persist_on = allow_persist && env_override("B200CONV_TC_PERSIST", 1) != 0;
+    if (persist_on && S == 1 && aligned && patch && tiles > num_sms() && gp.nbox == 1 &&
         ((int64_t)Wx * Wy * elem) % 16 == 0 && Ktot % BK == 0 && gp.tab_bytes > 0) {
         p->tma_f |= 32;                                    // bit 5: persistent CTAs
         p->grid_x = 1;
-        p->grid_y = kNumSMs;
+        p->grid_y = num_sms();
         p->grid_z = 1;
         p->block_x = kTpThreads;
     }
@@ -858,13 +852,8 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
                              const void *I, int C, int Wx, int Wy, const void *F, int K, int M,
                              float *O, int patch2d, cudaStream_t s, int N) {
     auto kern = kmtc_kernel<kTF32, BN, kTmaB, kPatch>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         p.smem_bytes);
+    cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
-    if (p.cluster_x > 8) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     const int BK = kTF32 ? 32 : 64;
     const int nkb = (int)(((int64_t)C * K * K + BK - 1) / BK);
     const int kb_per_split = (nkb + p.cluster_x - 1) / p.cluster_x;
@@ -882,13 +871,11 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    const char *dbgs = getenv("B200CONV_TC_DBG");
-    const int dbg = dbgs ? atoi(dbgs) : 0;
+    const int dbg = kDiag ? env_override("B200CONV_TC_DBG", 0) : 0;
     // split-K partials go through the L2 workspace (DSMEM reduction when the
     // workspace cannot grow during stream capture, or with B200CONV_TC_DSMEM=1)
     float *Wk = nullptr;
-    const char *dsm = getenv("B200CONV_TC_DSMEM");
-    if (p.cluster_x > 1 && !(dsm && dsm[0] == '1')) {
+    if (p.cluster_x > 1 && env_override("B200CONV_TC_DSMEM", 0) != 1) {
         const size_t bytes = (size_t)p.cluster_x * p.grid_y * p.grid_z * BN * kTcBM * 4;
         Wk = static_cast<float *>(workspace_get(bytes, s));
     }
@@ -899,12 +886,12 @@ template <bool kTF32, int BN>
 static cudaError_t launch_tc_persist(const conv_plan &p, const CUtensorMap &tf, const CUtensorMap &ti, int C, int Wx,
                                      int Wy, int K, int M, float *O, cudaStream_t s, int N) {
     auto kern = kmtc_persist_kernel<kTF32, BN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
     const int tiles_y = N * (((Wy - K + 1) * Wx + kTcBM - 1) / kTcBM);   // images x pixel tiles per image
     const int tiles = tiles_y * ((M + BN - 1) / BN);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(tiles < kNumSMs ? tiles : kNumSMs);
+    cfg.gridDim = dim3(tiles < num_sms() ? tiles : num_sms());
     cfg.blockDim = dim3(kTpThreads);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = s;
@@ -997,8 +984,7 @@ static cudaError_t launch_tc_prec(const conv_plan &p, const void *I, int C, int 
 
 int tc_max_clusters(int cluster, int smem) {
     auto kern = kmtc_kernel<true, 128, true, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_smem((const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster, 1, 1);
     cfg.blockDim = dim3(kTcThreads);

@@ -118,7 +118,8 @@ ks_kernel(const KsArgs a) {
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     const int RB = a.RWt * RR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool stamp = a.dbg && tid == 0 && blockIdx.x < 1024;
+    const int dbg = kDiag ? a.dbg : 0;
+    const bool stamp = dbg && tid == 0 && blockIdx.x < 1024;
     if (stamp) g_ks_stamps[4 * blockIdx.x] = gtimer();
 
     // this CTA's unit range -> task range -> row blocks and filter groups
@@ -253,14 +254,14 @@ ks_kernel(const KsArgs a) {
     }
     if (stamp) g_ks_stamps[4 * blockIdx.x + 2] = gtimer();
 
-    if (w0 >= w1 && !a.dbg) return;
+    if (w0 >= w1 && !dbg) return;
 
     const float *sin = s_in + pad - (int64_t)row_lo * Wx;   // sin[y*Wx + x] = I[y][x]
     const int64_t plane = (int64_t)Ho * Wo;
     float w[R * CKK];
     bool need_w = true;
     for (int u = w0; u < w1; ++u) {
-        const bool fine = a.dbg == 2 && blockIdx.x == 0 && threadIdx.x == 0 && u == w0;
+        const bool fine = dbg == 2 && blockIdx.x == 0 && threadIdx.x == 0 && u == w0;
         if (fine) g_ks_fine[0] = gtimer();
         if (need_w) {                                 // (warp-uniform) new task: load its taps
             need_w = false;
@@ -341,7 +342,7 @@ ks_kernel(const KsArgs a) {
             if (xv >= L) { xv -= L; ++rg; }
         }
     }
-    if (a.dbg) {
+    if (dbg) {
         __syncthreads();
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -434,8 +435,7 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
     // (measured, tools/ks_variants.py: 7x7 K=7 2.9 -> 2.2 us, 7x7 K=3 2.5 ->
     // 2.0 us, 28x28 K=3 2.24 -> 2.05 us; K >= 5 at 28x28 and K = 3 at 56x56
     // get slower).  B200CONV_KS_SMALL=<max Ho> overrides (0: off).
-    const char *sm = getenv("B200CONV_KS_SMALL");
-    const int small_ho = sm ? atoi(sm) : (K == 3 ? 32 : 16);
+    const int small_ho = kDiag ? env_override("B200CONV_KS_SMALL", K == 3 ? 32 : 16) : (K == 3 ? 32 : 16);
     const bool small = K >= 3 && Ho <= small_ho;
     const int TX = ks_TX(K), R = kC > 1 ? ks_R_c3(K) : ks_R(K), RR = small ? 1 : ks_RR(K);
     KsArgs a = {};
@@ -469,20 +469,18 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
     // (K = 1, pure store stream: one CTA per SM measured fastest — 9.4 vs
     // 11.5 us for 224x224 M=256 — fewer warps per SM keep the store traffic
     // fairer across SMs; see tools/ks_variants.py)
-    const int cap = (K == 1 ? 1 : (kC > 1 ? 2 : ks_min_blocks(K))) * kNumSMs;
+    const int cap = (K == 1 ? 1 : (kC > 1 ? 2 : ks_min_blocks(K))) * num_sms();
     const int max_smem = (kC == 1 && ks_min_blocks(K) == 3 ? 72 : 110) * 1024;
     // (B200CONV_KS_SPREAD=1: at least one CTA per SM up to one unit per CTA;
     // measured neutral on the small maps, so off by default)
     int G = (a.U + kKsWarps - 1) / kKsWarps;
-    if (const char *e = getenv("B200CONV_KS_SPREAD"); e && e[0] == '1') {
-        const int spread = a.U < kNumSMs ? a.U : kNumSMs;
+    if (kDiag && env_override("B200CONV_KS_SPREAD", 0) == 1) {
+        const int spread = a.U < num_sms() ? a.U : num_sms();
         if (G < spread) G = spread;
     }
     if (G > cap) G = cap;
-    if (const char *e = getenv("B200CONV_KS_G")) {        // experiments: CTA count override
-        const int g = atoi(e);
-        if (g > 0) G = g < a.U ? g : a.U;
-    }
+    if (const int g = kDiag ? env_override("B200CONV_KS_G", 0) : 0; g > 0)   // experiments: CTA count
+        G = g < a.U ? g : a.U;
     for (;;) {
         a.NW = G * kKsWarps;
         a.ub = a.U / a.NW;
@@ -550,10 +548,7 @@ static cudaLaunchAttribute pdl_attr() {
 template <int K, int VL, int VS, int RR = ks_RR(K)>
 static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
     auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R(K), RR>;
-    if (kp.smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.smem);
-        if (e != cudaSuccess) return e;
-    }
+    if (cudaError_t e = ensure_smem((const void *)kern, kp.smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kp.G);
     cfg.blockDim = dim3(kKsThreads);
@@ -563,10 +558,8 @@ static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     KsArgs a = kp.a;
-    const char *dbg = getenv("B200CONV_KS_DBG");
-    a.dbg = dbg ? atoi(dbg) : 0;
-    const char *pf = getenv("B200CONV_PREFETCH");
-    a.prefetch = !(pf && pf[0] == '0');
+    a.dbg = kDiag ? env_override("B200CONV_KS_DBG", 0) : 0;
+    a.prefetch = kDiag ? env_override("B200CONV_PREFETCH", 1) != 0 : 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
@@ -597,10 +590,7 @@ template <int K, int VL, int VS, typename T>
 static cudaError_t launch_ks_c3(const KsPlan &kp, cudaStream_t s) {
     constexpr int RR = ks_RR(K);
     auto kern = ks_kernel<K, ks_TX(K), VL, VS, ks_R_c3(K), RR, 3, T>;
-    if (kp.smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.smem);
-        if (e != cudaSuccess) return e;
-    }
+    if (cudaError_t e = ensure_smem((const void *)kern, kp.smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kp.G);
     cfg.blockDim = dim3(kKsThreads);
@@ -610,8 +600,7 @@ static cudaError_t launch_ks_c3(const KsPlan &kp, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     KsArgs a = kp.a;
-    const char *dbg = getenv("B200CONV_KS_DBG");
-    a.dbg = dbg ? atoi(dbg) : 0;
+    a.dbg = kDiag ? env_override("B200CONV_KS_DBG", 0) : 0;
     a.prefetch = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
@@ -631,8 +620,7 @@ static cudaError_t launch_ks_c3_v(const KsPlan &kp, cudaStream_t s) {
 }
 
 static bool c3_applies(int C, int K, int Wy) {
-    const char *e = getenv("B200CONV_C3");
-    if (e && e[0] == '0') return false;
+    if (env_override("B200CONV_C3", 1) == 0) return false;
     return C == 3 && (K == 3 || K == 5) && Wy - K + 1 > 16;   // (the 1-row small-map variant is not built)
 }
 

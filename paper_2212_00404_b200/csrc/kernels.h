@@ -8,7 +8,30 @@
 
 namespace b200 {
 
-constexpr int kNumSMs = 148;  // B200; planners size grids against it
+// SM count of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device; 148 on B200, and the fallback when no device is present, so plans
+// stay computable on a host without a GPU).  Planners size grids against it.
+int num_sms();
+
+// Diagnostic builds (-DB200CONV_DIAG, `python -m paper_2212_00404_b200.build
+// --diag` -> libb200conv_diag.so) compile the timeline stamps and the work-
+// skipping switches of B200CONV_{KS,SIMT,TC}_DBG; the product library has
+// none of them (the kernels see dbg == 0 as a constant).
+#ifdef B200CONV_DIAG
+constexpr bool kDiag = true;
+#else
+constexpr bool kDiag = false;
+#endif
+
+// Documented planner overrides (include/b200conv.h "Planner overrides"): an
+// integer environment variable, or `def` when unset.  They only choose among
+// correct plans (tests force every path with them); read at each call.
+int env_override(const char *name, int def);
+
+// Raise a kernel's dynamic shared memory limit to at least `bytes` (and allow
+// non-portable cluster sizes).  The limit only ever grows, under a mutex, so a
+// concurrent launch of the same kernel with a smaller footprint never fails.
+cudaError_t ensure_smem(const void *kernel, int bytes);
 
 // Programmatic dependent launch on/off (env B200CONV_PDL=0 disables it).
 int pdl_enabled();
@@ -57,9 +80,19 @@ int choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_u
 // co-resident clusters of size S (1..16) for 1 or 2 CTAs per SM (same table)
 int clusters_resident(int S, int ctas_per_sm);
 
+// Every ABI entry point holds a CallScope for the duration of the call: the
+// graph-private scratch allocated while a stream is being captured is freed
+// (cudaFreeAsync, in stream order) when the outermost scope ends.
+struct CallScope {
+    CallScope();
+    ~CallScope();
+    CallScope(const CallScope &) = delete;
+    CallScope &operator=(const CallScope &) = delete;
+};
+
 // split-K workspace (workspace.cu): >= bytes of device memory owned by the
-// library for (current device, stream); nullptr if it would have to grow
-// while the stream is being captured (or on OOM)
+// library for (current device, stream); during stream capture a graph memory
+// allocation private to the captured graph (needs a CallScope); nullptr on OOM
 void *workspace_get(size_t bytes, cudaStream_t s);
 // zero-padded input copies (padded calls): a second per-(device, stream) buffer
 void *padbuf_get(size_t bytes, cudaStream_t s);

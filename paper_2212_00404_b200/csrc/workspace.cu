@@ -11,10 +11,12 @@
 // O[M][Ho*Wo].
 //
 // The workspace is owned by the library: one buffer per (device, stream),
-// grown (never shrunk, old buffers retired but kept alive) on demand outside
-// stream capture; a call made while the stream is being captured that would
-// need a bigger buffer gets nullptr and the caller falls back to a plan that
-// needs none (cluster / DSMEM reduction).
+// grown (never shrunk, old buffers retired but kept alive) on demand.  A call
+// made while its stream is being captured into a CUDA graph never touches
+// these shared buffers: its scratch is a graph memory allocation
+// (cudaMallocAsync inside the capture, freed by cudaFreeAsync after the
+// call's last kernel), private to that graph, so graphs captured on the same
+// stream can be replayed concurrently.
 #include <cstdint>
 #include <cstdlib>
 #include <map>
@@ -34,7 +36,18 @@ std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_pad;
 std::map<std::pair<int, cudaStream_t>, WsBuf> g_aux;
 std::vector<void *> g_ws_retired;
+// graph-private scratch of the calls being captured on this thread, released
+// when the outermost entry point returns
+thread_local std::vector<std::pair<void *, cudaStream_t>> t_graph_scratch;
+thread_local int t_call_depth = 0;
 }  // namespace
+
+CallScope::CallScope() { ++t_call_depth; }
+CallScope::~CallScope() {
+    if (--t_call_depth > 0) return;
+    for (auto &ps : t_graph_scratch) cudaFreeAsync(ps.first, ps.second);
+    t_graph_scratch.clear();
+}
 
 static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, size_t bytes, cudaStream_t s);
 
@@ -51,12 +64,19 @@ void *auxbuf_get(size_t bytes, cudaStream_t s) { return buffer_get(g_aux, bytes,
 static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, size_t bytes, cudaStream_t s) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (cs != cudaStreamCaptureStatusNone) {
+        // graph-private scratch (a memory node of the captured graph)
+        if (t_call_depth == 0) return nullptr;
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        t_graph_scratch.emplace_back(p, s);
+        return p;
+    }
     std::lock_guard<std::mutex> lk(g_ws_mu);
     WsBuf &b = pool[{dev, s}];
     if (b.bytes >= bytes) return b.p;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-    if (cs != cudaStreamCaptureStatusNone) return nullptr;
     // The old buffer is retired, not freed: in-flight work, or a CUDA graph
     // captured earlier on this stream, may still reference it.  Growth is
     // geometric, so retired buffers total less than the live one.
@@ -159,7 +179,7 @@ pad_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restri
 cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s) {
     const int64_t total = (int64_t)NC * (Wy + 2 * pad) * (Wx + 2 * pad);
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks));
     cfg.blockDim = dim3(256);
@@ -193,7 +213,7 @@ pad_rows_kernel(const T *__restrict__ F, int M, int Ktot, int Kp, T *__restrict_
 cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, void *Fp, cudaStream_t s) {
     const int64_t total = (int64_t)M * Kp;
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks));
     cfg.blockDim = dim3(256);
@@ -214,11 +234,11 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
                                  cudaStream_t s, int plane) {
     if (plane <= 0) plane = N;
     // few splits: one lane per float4 of outputs; many: 8 lanes (latency)
-    const char *e = getenv("B200CONV_REDG");
-    const int G = e ? atoi(e) : (S > 16 ? 8 : 1);
+    const int Gd = S > 16 ? 8 : 1;
+    const int G = kDiag ? (env_override("B200CONV_REDG", Gd) == 8 ? 8 : 1) : Gd;
     const int64_t total = (int64_t)M * ((N + 3) / 4);
     int64_t blocks = (total * G + 255) / 256;          // one float4 group per G lanes
-    if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;        // grid-stride: CTA launch rate, not work, bounds tiny CTAs
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();        // grid-stride: CTA launch rate, not work, bounds tiny CTAs
     if (blocks < 1) blocks = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
-    assert conv.version() == (1 << 16) | 5
+    assert conv.version() == (1 << 16) | 6
 
 
 def test_status_strings():
@@ -171,3 +171,36 @@ def test_strided_argument_errors_and_plans():
             Ho = (W + 2 * pad - K) // s + 1
             if kern == 1:
                 assert p["grid_y"] * p["tile_n"] >= Ho * Ho        # compact pixel tiles cover the strided map
+
+
+def test_strided_output_overflow_is_a_shape_error_before_any_device_work():
+    lib = conv.load()
+    f = 0x1000
+    # N*C*Wx*Wy = 2^30 fits, N*M*Ho*Wo = 2^42 does not: rejected before the pad pre-pass
+    assert lib.conv_multi_strided_ex(f, 1 << 14, 1, 256, 256, f, 1, 1 << 14, 1, 2, f, 0, None) == 1
+
+
+@pytest.mark.parametrize("call", [
+    lambda: conv.single(torch.zeros(8, 8), torch.zeros(2, 3, 3)),                                 # CPU tensors
+    lambda: conv.multi_host(torch.zeros(3, 8, 8), torch.zeros(4, 2, 3, 3)),                       # channels
+    lambda: conv.multi_host(torch.zeros(3, 8, 8).bfloat16(), torch.zeros(4, 3, 3, 3).bfloat16()),  # dtype vs fp32
+    lambda: conv.single_host(torch.zeros(8, 8, dtype=torch.float64), torch.zeros(2, 3, 3)),       # dtype
+    lambda: conv.single_host(torch.zeros(8, 16)[:, ::2], torch.zeros(2, 3, 3)),                   # non-contiguous
+    lambda: conv.multi_host(torch.zeros(3, 8, 8), torch.zeros(4, 3, 3, 3), out=torch.zeros(4, 6, 5)),  # out shape
+    lambda: conv.single_host(torch.zeros(8, 8), torch.zeros(2, 3, 2)),                            # non-square F
+    lambda: conv.single_host(torch.zeros(4, 4), torch.zeros(2, 5, 5)),                            # K > map
+])
+def test_python_conveniences_validate_before_the_abi(call):
+    with pytest.raises((ValueError, TypeError)):
+        call()
+
+
+def test_verify_cli_usage_and_infeasible_exit_codes():
+    import subprocess
+    import sys
+    v = os.path.join(ROOT, "tests", "verify.py")
+    run = lambda *a: subprocess.run([sys.executable, v, *a], capture_output=True, text=True).returncode
+    assert run("--mode", "multi") == 1                                                  # usage
+    assert run("--mode", "single", "--wx", "8", "--wy", "8", "--k", "3", "--m", "2", "--c", "3") == 1
+    assert run("--mode", "multi", "--wx", "4", "--wy", "4", "--c", "2", "--k", "5", "--m", "2") == 2
+    assert run("--help") == 0

@@ -185,3 +185,16 @@ def test_sharded_path_two_processes_end_to_end():
         for r in (0, 1):
             check(res[r][prec], Oo, A, TAU[prec], f"rank {r} gathered {prec}")
         assert np.array_equal(res[0][prec], res[1][prec])
+
+
+@pytest.mark.parametrize("args", [
+    ["--mode", "single", "--wx", "224", "--wy", "224", "--k", "3", "--m", "64"],
+    ["--mode", "multi", "--wx", "14", "--wy", "14", "--c", "512", "--k", "3", "--m", "4096", "--precision", "bf16"],
+    ["--mode", "multi", "--wx", "27", "--wy", "27", "--c", "96", "--k", "5", "--m", "256", "--precision", "tf32"],
+])
+def test_verify_cli_passes(conv, args):
+    import subprocess
+    import sys
+    v = os.path.join(os.path.dirname(os.path.abspath(__file__)), "verify.py")
+    r = subprocess.run([sys.executable, v, *args], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("PASS"), r.stdout + r.stderr

@@ -6,6 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
 from paper_2212_00404_b200 import conv
+from paper_2212_00404_b200 import build as _b
+conv.load(_b.build(diag=True))       # the -DB200CONV_DIAG library (stamps / DBG switches)
 dev = torch.device("cuda", 0)
 args = [int(a) for a in sys.argv[1:]]
 lib = conv.load()

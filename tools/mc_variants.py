@@ -31,7 +31,7 @@ def timeit(fn, reps=12):
 
 
 for want in sys.argv[2:]:
-    for c in bench.suite():
+    for c in bench.suite_calls(1, 0):
         if want not in c["label"] or c["kind"] != "multi":
             continue
         dt = torch.bfloat16 if c["prec"] == "bf16" else torch.float32

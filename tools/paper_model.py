@@ -25,11 +25,11 @@ print(f"B200: N_FMA = {N_FMA:,} FMAs per SM per data set (paper's x2 convention:
       f" = {V_S / SMS / 16:.0f} 16-B loads per SM ({V_S / SMS / 4:.0f} 4-B loads > 2048 threads:"
       f" the paper's one-word-per-thread rule cannot cover HBM latency on B200 — 16-B vectors / TMA bulk copies do)")
 rows = []
-for c in bench.suite():
+for c in bench.suite_calls(1, 0):
     fma = c["flop"] / 2
     per_sm = fma / SMS
     method = "1 (prefetch / compute)" if per_sm >= N_FMA else "2 (bandwidth / latency)"
-    rows.append((c["label"], fma, per_sm / N_FMA, method, bench.roof_for(c, pk)[0]))
+    rows.append((c["label"], fma, per_sm / N_FMA, method, bench.roof(c, c["prec"], "KS" if c["kind"] == "single" else "KM", pk, SMS)[0]))
 print(f"{'layer':38s} {'FMA':>12s} {'FMA/SM / N_FMA':>15s}  paper's method           roofline bound")
 for r in rows:
     if r[0].startswith("single") and not r[0].startswith(("single_224", "single_56x56_k7")):

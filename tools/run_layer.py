@@ -9,7 +9,7 @@ from paper_2212_00404_b200 import conv
 want = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 dev = torch.device("cuda", 0)
-for c in bench.suite():
+for c in bench.suite_calls(1, 0):
     if want not in c["label"]:
         continue
     dt = torch.bfloat16 if c["prec"] == "bf16" else torch.float32

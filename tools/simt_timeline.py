@@ -5,10 +5,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import bench, synth
 from paper_2212_00404_b200 import conv
+from paper_2212_00404_b200 import build as _b
+conv.load(_b.build(diag=True))       # the -DB200CONV_DIAG library (stamps / DBG switches)
 dev = torch.device("cuda", 0)
 lib = conv.load()
 for want in sys.argv[1:]:
-    for c in bench.suite():
+    for c in bench.suite_calls(1, 0):
         if want not in c["label"] or c["prec"] != "fp32" or c["kind"] != "multi":
             continue
         I = torch.from_numpy(synth.uniform01(synth.SEED_I, (c["C"], c["Wy"], c["Wx"]))).to(dev)

@@ -8,9 +8,11 @@ sys.path.insert(0, '{os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.environ['B200CONV_TC_DBG'] = '{dbg}'
 import torch, bench, synth
 from paper_2212_00404_b200 import conv
+from paper_2212_00404_b200 import build as _b
+conv.load(_b.build(diag=True))       # the -DB200CONV_DIAG library (stamps / DBG switches)
 dev = torch.device('cuda', 0)
 r = {{}}
-for c in bench.suite():
+for c in bench.suite_calls(1, 0):
     if c['kind'] != 'multi' or c['prec'] == 'fp32': continue
     if not any(n in c['name'] for n in ('sweep', 'target', 'resnet_7')): continue
     dt = torch.bfloat16 if c['prec'] == 'bf16' else torch.float32

@@ -2,6 +2,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np, synth
 from paper_2212_00404_b200 import conv
+from paper_2212_00404_b200 import build as _b
+conv.load(_b.build(diag=True))       # the -DB200CONV_DIAG library (stamps / DBG switches)
 dbg = sys.argv[1]
 os.environ['B200CONV_TC_DBG'] = dbg
 dev = torch.device('cuda', 0)

@@ -5,6 +5,8 @@ import os, sys, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
 from paper_2212_00404_b200 import conv
+from paper_2212_00404_b200 import build as _b
+conv.load(_b.build(diag=True))       # the -DB200CONV_DIAG library (stamps / DBG switches)
 N, prec = int(sys.argv[1]), sys.argv[2]
 os.environ["B200CONV_TC_DBG"] = os.environ.get("STAMP_DBG", "128")
 dev = torch.device("cuda", 0)
