@@ -30,14 +30,15 @@
  * calls: one device buffer each per (device, stream), grown on demand
  * (geometric growth; superseded buffers stay allocated, since work in flight
  * may still reference them) and kept for the process lifetime.  A call made
- * while its stream is being captured into a CUDA graph does not use those
- * shared buffers: its scratch is a graph memory allocation (cudaMallocAsync
+ * while its stream is being captured into a CUDA graph bakes in that stream's
+ * buffer if it is big enough, else a graph memory allocation (cudaMallocAsync
  * node before its kernels, cudaFreeAsync node after them) private to the
- * captured graph, so graphs captured on one stream may be replayed
- * concurrently on different streams.  Two threads issuing calls on the SAME
- * stream handle (e.g. cudaStreamPerThread is one value for all threads, or
- * the legacy stream) share that stream's buffers: such calls must be ordered
- * by the stream itself, as any work on one stream is.  The *_host entry
+ * graph.  Hence: graphs captured on the SAME stream may share scratch and must
+ * be replayed in stream order (not concurrently on different streams); to
+ * replay graphs concurrently, capture them on different streams.  Likewise
+ * two threads issuing calls on the same stream handle (cudaStreamPerThread is
+ * one value for all threads; the legacy stream) share its buffers and must be
+ * ordered by that stream, as any work on one stream is.  The *_host entry
  * points take host pointers and use a library-owned stream-ordered memory
  * pool.  O must not overlap I or F.
  *

@@ -52,9 +52,11 @@ _lock = threading.Lock()
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load the C-ABI library (raises if it was not built — no fallback)."""
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load the C-ABI library (raises if it was not built — no fallback).
+    B200CONV_LIB_PATH selects another build of it (A/B measurements)."""
     global _lib
+    path = path or os.environ.get("B200CONV_LIB_PATH") or LIB_PATH
     with _lock:
         if _lib is None:
             if not os.path.exists(path):

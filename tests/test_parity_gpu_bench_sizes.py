@@ -198,3 +198,33 @@ def test_verify_cli_passes(conv, args):
     v = os.path.join(os.path.dirname(os.path.abspath(__file__)), "verify.py")
     r = subprocess.run([sys.executable, v, *args], capture_output=True, text=True)
     assert r.returncode == 0 and r.stdout.startswith("PASS"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("prec,layer", [("fp32", 7), ("tf32", 2), ("bf16", 7)])
+def test_capture_on_a_fresh_stream_uses_graph_private_scratch(conv, prec, layer):
+    """A workspace-needing call captured on a stream that never ran it (its
+    buffer cannot grow during capture) gets graph memory-node scratch; two
+    such graphs replayed on different streams at once stay correct."""
+    c = (list(synth.MULTI_LAYERS) + [synth.SHARD_SWEEP])[layer]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=500 + layer)
+    Id, Fd = torch.from_numpy(I).cuda().to(_dt(prec)), torch.from_numpy(F).cuda().to(_dt(prec))
+    ref = conv.multi(Id, Fd, prec)
+    shape = tuple(ref.shape)
+    outs, graphs, streams = [], [], [torch.cuda.Stream(), torch.cuda.Stream()]
+    for st in streams:
+        O = torch.full(shape, float("nan"), device="cuda")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            g.capture_begin()
+            conv.conv_multi_ex(Id, c["C"], c["Wx"], c["Wy"], Fd, c["K"], c["M"], O, prec, st.cuda_stream)
+            g.capture_end()
+        outs.append(O)
+        graphs.append(g)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for st, g in zip(streams, graphs):
+            with torch.cuda.stream(st):
+                g.replay()
+    torch.cuda.synchronize()
+    for O in outs:
+        assert torch.equal(O, ref)
