@@ -353,6 +353,23 @@ bool encode_2d(CUtensorMap *m, bool tf32, const void *base, uint64_t inner, uint
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+}  // namespace
+
+bool encode_f32_2d_plain(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                         uint32_t box_inner, uint32_t box_outer) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    memset(m, 0, sizeof(*m));
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
 // pixel-side tile width (mode F: N of the MMA): the smallest instantiated
 // width >= n (every X byte a CTA streams is TMA ingest, ~53 B/clk per SM)
 int round_bn(int n) {

@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -79,9 +80,10 @@ kmn_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     }
 }
 
-// smem layout (floats): F_s[CK][BM] | B_s[2][CK][BN] | Fraw[BM][RS] | koff[CK] (int)
-// (F is double buffered through Fraw: chunk c+1 lands in Fraw while chunk c
-// computes from F_s, and is transposed into F_s once every thread is done.)
+// smem layout (floats): F[2][BM][RS] | B[2][CKP][BN] | koff[CKP] (int): a
+// two-stage ring of (F rows as stored, im2col tile); CKP = the chunk's k padded
+// to whole 16-B quads.  The main loop reads F in place, four k per 16-B load
+// (no transpose pass), and issues paired FMAs (FFMA2, ptx.cuh ffma2).
 __host__ __device__ constexpr int simt_rs(int CK) { return ((CK - 4 + 31) / 32) * 32 + 4; }
 
 // Thread tile: 8 filters (two 4-row halves, BM/2 apart) x TN pixels, TN in
@@ -95,12 +97,13 @@ struct SimtShape {
     static constexpr int R1 = 4 * TNG;
     static constexpr int T2 = TN - 4;               // 0, 2 or 4
     static_assert(TMG * TNG == kSimtThreads && TNG * TN == BN, "tile must map to 256 threads");
-    __device__ static int row(int tm, int i) { return i < 4 ? tm * 4 + i : BM / 2 + tm * 4 + (i - 4); }
+    __device__ static int row(int tm, int i) { return tm + TMG * i; }     // interleaved thread rows
 };
 
-template <int BM, int BN, int TN>
+template <int BM, int BN, int TN, bool kTmaF>
 __global__ void __launch_bounds__(kSimtThreads, 2)
-kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__restrict__ F,
+kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ I, int C, int Wx, int Wy,
+           const float *__restrict__ F,
            int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg_in,
            int sd, int Nimg) {
     using SH = SimtShape<BM, BN, TN>;
@@ -118,13 +121,18 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int Ptot = Nimg * HoWo;                   // compact pixels of all images (batch)
     const int Ktot = C * KK;
     const int CK = CB * KK;
-    const int RS = simt_rs(CK);
 
-    extern __shared__ __align__(16) float smem[];
-    float *Fs_buf = smem;                           // [CK][BM]
-    float *Bs_buf = smem + CK * BM;                 // [2][CK][BN]
-    float *Fraw = Bs_buf + 2 * CK * BN;             // [BM][RS]
-    int *koff = reinterpret_cast<int *>(Fraw + BM * RS);   // [CK]
+    const int CKP = (CK + 3) & ~3;                  // k per chunk, padded to whole 16-B quads
+    // F row stride: RS = 4 mod 32 words (cp.async rows); TMA boxes land dense
+    // (CKP = CK, CK / 4 not a multiple of 4: consecutive rows still hit
+    // different 16-B bank quads)
+    const int RS = kTmaF ? CKP : simt_rs(CKP);
+
+    extern __shared__ __align__(128) float smem[];
+    float *Fst = smem;                              // [2][BM][RS]   F rows as stored (k fastest)
+    float *Bst = smem + 2 * BM * RS;                // [2][CKP][BN]  im2col tile
+    int *koff = reinterpret_cast<int *>(Bst + 2 * CKP * BN);   // [CKP]
+    uint64_t *fbar = reinterpret_cast<uint64_t *>(koff + ((CKP + 1) & ~1));   // [2] F stage barriers (TMA)
 
     const int S = gridDim.x;                        // split count (== cluster size when W == nullptr)
     const int split = blockIdx.x;
@@ -144,9 +152,9 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     const int vw = fits(4) ? 4 : (fits(2) ? 2 : 1);
 
     // k -> input offset within a chunk (channel relative to the chunk start)
-    for (int k = tid; k < CK; k += NT) {
+    for (int k = tid; k < CKP; k += NT) {
         const int ch = k / KK, rem = k - ch * KK, r = rem / K;
-        koff[k] = ch * HW + r * Wx + (rem - r * K);
+        koff[k] = k < CK ? ch * HW + r * Wx + (rem - r * K) : 0;
     }
     // this thread's im2col pixel (fixed for the whole kernel) and k-lane
     constexpr int KL = NT / BN > 0 ? NT / BN : 1;
@@ -159,74 +167,66 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
     // input pixel of output (by, bx) of image bimg
     const int64_t bbase = (int64_t)bimg * C * HW + sd * (by * Wx + (bpix - by * Wo));
 
-    // F rows: thread -> fixed vector column v of rows mr, mr + rpt, ... (chunk
-    // invariant, decoded once)
-    const int f_nv = CK / vw;
-    const int f_rpt = NT / f_nv;
-    const bool f_act = tid < f_nv * f_rpt;
-    const int f_v = f_act ? tid % f_nv : 0, f_mr = f_act ? tid / f_nv : 0;
-    const uint32_t f_dst0 = smem_u32(Fraw + f_mr * RS + vw * f_v);
-    const int64_t f_src0 = (int64_t)(m0 + f_mr) * Ktot + vw * f_v;
-    auto load_f = [&](int chunk) {
+    // F rows straight into Fst[stage][m][0..CKP): thread -> fixed vector column
+    // v (+ NT, ... when a row has more than NT vectors) of rows mr, mr + rpt, ...
+    // (chunk invariant, decoded once); columns past the chunk's valid k and
+    // rows past M are zero-filled
+    const int f_nv = CKP / vw;
+    const int f_rpt = NT / f_nv > 0 ? NT / f_nv : 1;
+    const int f_vstep = f_nv < NT ? f_nv : NT;
+    const bool f_act = tid < f_vstep * f_rpt;
+    const int f_v = f_act ? tid % f_vstep : 0, f_mr = f_act ? tid / f_vstep : 0;
+    const int64_t f_step = (int64_t)f_rpt * Ktot;
+    auto load_f = [&](int chunk, int st) {
+        if constexpr (kTmaF) {
+            // one 2-D TMA box [BM rows][CK k] of F seen as [M][Ktot]: rows past
+            // M and k past Ktot (the last, partial chunk) are zero-filled
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&fbar[st], BM * CKP * 4);
+                tma_load_2d(Fst + st * BM * RS, &tmapF, &fbar[st], (ch_begin + chunk * CB) * KK, m0);
+            }
+            return;
+        }
         if (!f_act) return;
         const int ch0 = ch_begin + chunk * CB;
         const int nk = min(CB, ch_end - ch0) * KK;            // valid k of this chunk
-        const bool kok = vw * f_v < nk;                       // nk is a multiple of vw
-        const float *src = F + f_src0 + (int64_t)ch0 * KK;
-        uint32_t dst = f_dst0;
-        for (int m = f_mr; m < BM; m += f_rpt) {
-            const bool ok = kok && (m0 + m < M);
-            const float *sp = ok ? src : F;
-            if (vw == 4)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
-                             ::"r"(dst), "l"(sp), "r"(ok ? 16 : 0) : "memory");
-            else if (vw == 2)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
-                             ::"r"(dst), "l"(sp), "r"(ok ? 8 : 0) : "memory");
-            else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
-                             ::"r"(dst), "l"(sp), "r"(ok ? 4 : 0) : "memory");
-            src += (int64_t)f_rpt * Ktot;
-            dst += f_rpt * RS * 4;
+        const uint32_t dstep = f_rpt * RS * 4;
+        for (int v = f_v; v < f_nv; v += f_vstep) {
+            const bool kok = vw * v < nk;                     // nk is a multiple of vw
+            const float *src = F + (int64_t)(m0 + f_mr) * Ktot + (int64_t)ch0 * KK + vw * v;
+            uint32_t dst = smem_u32(Fst + st * BM * RS + f_mr * RS + vw * v);
+            // (one loop per copy width: no per-element width branch)
+            if (vw == 4) {
+                for (int m = f_mr; m < BM; m += f_rpt, src += f_step, dst += dstep) {
+                    const bool ok = kok && m0 + m < M;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                                 ::"r"(dst), "l"(ok ? src : F), "r"(ok ? 16 : 0) : "memory");
+                }
+            } else if (vw == 2) {
+                for (int m = f_mr; m < BM; m += f_rpt, src += f_step, dst += dstep) {
+                    const bool ok = kok && m0 + m < M;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                                 ::"r"(dst), "l"(ok ? src : F), "r"(ok ? 8 : 0) : "memory");
+                }
+            } else {
+                for (int m = f_mr; m < BM; m += f_rpt, src += f_step, dst += dstep) {
+                    const bool ok = kok && m0 + m < M;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                                 ::"r"(dst), "l"(ok ? src : F), "r"(ok ? 4 : 0) : "memory");
+                }
+            }
         }
     };
     // im2col tile B[k][n] = I[ch0 + ch][y_n + r][x_n + c] (zero past the valid range)
-    auto load_b = [&](int chunk, int b) {
+    auto load_b = [&](int chunk, int st) {
         if (bkl >= KL) return;
         const int ch0 = ch_begin + chunk * CB;
         const int nk = bvalid ? min(CB, ch_end - ch0) * KK : 0;
         const float *src = I + (int64_t)ch0 * HW + bbase;
-        uint32_t dst = smem_u32(Bs_buf + b * CK * BN + bkl * BN + bn);
+        uint32_t dst = smem_u32(Bst + st * CKP * BN + bkl * BN + bn);
 #pragma unroll 4
-        for (int k = bkl; k < CK; k += KL, dst += KL * BN * 4)
+        for (int k = bkl; k < CKP; k += KL, dst += KL * BN * 4)
             cp_async4_zf(dst, src + koff[k], k < nk);    // k >= nk: zero fill, src not read
-    };
-    // Fraw[m][k..k+3] (16-B loads along m: RS == 4 mod 32 -> conflict-free)
-    //   -> F_s[k+i][m] (scalar stores, consecutive m -> conflict-free)
-    auto transpose_f = [&]() {
-        float *fs = Fs_buf;
-        if (CK % 4 == 0) {
-            // thread -> fixed m, quads q0, q0 + QS, ...: pointer increments only
-            constexpr int QS = NT / BM;
-            const int m = tid % BM, q0 = tid / BM;
-            const float *src = Fraw + m * RS + 4 * q0;
-            float *dst = fs + 4 * q0 * BM + m;
-#pragma unroll 4
-            for (int q = q0; q < CK / 4; q += QS, src += 4 * QS, dst += 4 * QS * BM) {
-                const float4 v = *reinterpret_cast<const float4 *>(src);
-                dst[0] = v.x; dst[BM] = v.y; dst[2 * BM] = v.z; dst[3 * BM] = v.w;
-            }
-            return;
-        }
-        const int nq = (CK + 3) / 4;
-        for (int u = tid; u < BM * nq; u += NT) {
-            const int m = u % BM, q = u / BM;
-            const float4 v = *reinterpret_cast<const float4 *>(Fraw + m * RS + 4 * q);
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (4 * q + i < CK) fs[(4 * q + i) * BM + m] = vv[i];
-        }
     };
 
     float acc[8][TN];
@@ -235,55 +235,63 @@ kms_kernel(const float *__restrict__ I, int C, int Wx, int Wy, const float *__re
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
+    if (kTmaF && tid == 0) {
+        tma_prefetch_desc(&tmapF);
+        mbar_init(&fbar[0], 1);
+        mbar_init(&fbar[1], 1);
+        fence_mbar_init();
+    }
     pdl_wait();
     pdl_trigger();
     if (tl) g_simt_cta[5 * cta_lin + 1] = simt_gtimer();
-    __syncthreads();                                // koff table
-    if (nchunks > 0) {
-        load_f(0);
-        load_b(0, 0);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        if (tl) g_simt_cta[5 * cta_lin + 2] = simt_gtimer();
-        transpose_f();
-        __syncthreads();
-        if (nchunks > 1) { load_f(1); load_b(1, 1); }
-        cp_async_commit();
-    }
+    __syncthreads();                                // koff table, barriers
+    // two-stage ring: chunk c lives in stage c & 1; chunk c + 1 is in flight
+    // while chunk c computes (the paper's prefetch rounds)
+    if (nchunks > 0) { load_f(0, 0); load_b(0, 0); }
+    cp_async_commit();
+    if (nchunks > 1) { load_f(1, 1); load_b(1, 1); }
+    cp_async_commit();
     for (int chunk = 0; chunk < nchunks; ++chunk) {
-        const int b = chunk & 1;
-        const float *Fs = Fs_buf + tm * 4;
-        const float *Bs = Bs_buf + b * CK * BN + tn * 4;
-        const float *Bs2 = Bs_buf + b * CK * BN + SH::R1 + tn * T2;
-#pragma unroll 4
-        for (int k = 0; k < CK; ++k) {
-            const float4 a0 = *reinterpret_cast<const float4 *>(Fs + k * BM);
-            const float4 a1 = *reinterpret_cast<const float4 *>(Fs + k * BM + BM / 2);
-            const float4 b0 = *reinterpret_cast<const float4 *>(Bs + k * BN);
-            float bv[TN];
-            bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
-            if constexpr (T2 == 4) {
-                const float4 b1 = *reinterpret_cast<const float4 *>(Bs2 + k * BN);
-                bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
-            } else if constexpr (T2 == 2) {
-                const float2 b1 = *reinterpret_cast<const float2 *>(Bs2 + k * BN);
-                bv[4] = b1.x; bv[5] = b1.y;
+        const int st = chunk & 1;
+        cp_async_wait<1>();                         // chunk c staged (c + 1 may be in flight)
+        __syncthreads();
+        if constexpr (kTmaF) mbar_wait(&fbar[st], (chunk >> 1) & 1);
+        if (tl && chunk == 0) g_simt_cta[5 * cta_lin + 2] = simt_gtimer();
+        // A = F rows in place: thread rows tm + i * TMG (consecutive rows across
+        // the warp's lanes: conflict-free 16-B loads along k), four k per load;
+        // B = the im2col tile, TN consecutive pixels per k
+        const float *Fa = Fst + st * BM * RS + tm * RS;
+        const float *Bs = Bst + st * CKP * BN + tn * 4;
+        const float *Bs2 = Bst + st * CKP * BN + SH::R1 + tn * T2;
+#pragma unroll 1
+        for (int kq = 0; kq < CKP; kq += 4) {
+            float4 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(Fa + i * SH::TMG * RS + kq);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int k = kq + kk;
+                const float4 b0 = *reinterpret_cast<const float4 *>(Bs + k * BN);
+                float bv[TN];
+                bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
+                if constexpr (T2 == 4) {
+                    const float4 b1 = *reinterpret_cast<const float4 *>(Bs2 + k * BN);
+                    bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
+                } else if constexpr (T2 == 2) {
+                    const float2 b1 = *reinterpret_cast<const float2 *>(Bs2 + k * BN);
+                    bv[4] = b1.x; bv[5] = b1.y;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float ai = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+                    for (int j = 0; j < TN; j += 2) ffma2(acc[i][j], acc[i][j + 1], ai, bv[j], bv[j + 1]);
+                }
             }
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
-        if (chunk + 1 < nchunks) {
-            cp_async_wait<0>();                     // chunk c+1 staged
-            __syncthreads();                        // ... and everyone is done with chunk c
-            transpose_f();
-            __syncthreads();
-            if (chunk + 2 < nchunks) { load_f(chunk + 2); load_b(chunk + 2, b); }
-            cp_async_commit();
-        }
+        __syncthreads();                            // every thread is done with stage st
+        if (chunk + 2 < nchunks) { load_f(chunk + 2, st); load_b(chunk + 2, st); }
+        cp_async_commit();
     }
     cp_async_wait<0>();
     if (tl) g_simt_cta[5 * cta_lin + 3] = simt_gtimer();
@@ -366,7 +374,8 @@ constexpr SimtTile kSimtTiles[kNumSimtTiles] = {
     {256, 32, 4}, {128, 64, 4}, {64, 128, 4}};
 
 int simt_smem(int BM, int BN, int CK) {
-    const int bytes = (CK * BM + 2 * CK * BN + BM * simt_rs(CK)) * 4 + CK * 4;
+    const int CKP = (CK + 3) & ~3;
+    const int bytes = (2 * BM * simt_rs(CKP) + 2 * CKP * BN) * 4 + ((CKP + 1) & ~1) * 4 + 16;
     const int pbytes = BM * BN * 4;
     return bytes > pbytes ? bytes : pbytes;
 }
@@ -526,11 +535,26 @@ int plan_multi_simt(int C, int Wx, int Wy, int K, int M, conv_plan *p, int sd, i
     return 0;
 }
 
+// F rows by TMA when the chunk is a whole number of 16-B quads that lands
+// bank-conflict-free densely and F rows are 16-B strided
+bool simt_tma_f(const float *F, int C, int K, int CB) {
+    const int KK = K * K, CK = CB * KK;
+    return (C * KK) % 4 == 0 && CK % 4 == 0 && CK <= 256 && (CK / 4) % 4 != 0 &&
+           reinterpret_cast<uintptr_t>(F) % 16 == 0;
+}
+
 template <int BM, int BN, int TN>
 static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float *I, int C, int Wx, int Wy,
                               const float *F, int K, int M, float *O, float *W, cudaStream_t s, int sd,
                               int Nimg) {
-    auto kern = kms_kernel<BM, BN, TN>;
+    CUtensorMap tmap;
+    bool tma = simt_tma_f(F, C, K, c.CB);
+    if (tma) {
+        const int CK = c.CB * K * K;
+        tma = encode_f32_2d_plain(&tmap, F, (uint64_t)C * K * K, (uint64_t)M, (uint64_t)C * K * K * 4, CK, BM);
+    }
+    if (!tma) memset(&tmap, 0, sizeof(tmap));
+    auto kern = tma ? kms_kernel<BM, BN, TN, true> : kms_kernel<BM, BN, TN, false>;
     cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -548,7 +572,7 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     cfg.attrs = attr;
     cfg.numAttrs = W ? 1 : 2;
     const int dbg = kDiag ? env_override("B200CONV_SIMT_DBG", 0) : 0;
-    e = cudaLaunchKernelEx(&cfg, kern, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd, Nimg);
+    e = cudaLaunchKernelEx(&cfg, kern, tmap, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd, Nimg);
     if (e != cudaSuccess || !W) return e;
     const int ldw = p.grid_y * BN;
     const int64_t slice = (int64_t)p.grid_z * BM * ldw;
@@ -557,7 +581,7 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
 }
 
 int simt_max_clusters(int cluster, int smem) {
-    auto kern = kms_kernel<128, 128, 8>;
+    auto kern = kms_kernel<128, 128, 8, false>;
     ensure_smem((const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster, 1, 1);

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "../../include/b200conv.h"
 
@@ -106,6 +107,11 @@ cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem,
 // a batch, column n is pixel n % plane of image n / plane, O [N/plane][M][plane]
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
                                  cudaStream_t s, int plane = 0);
+
+// 2-D FP32 tensor map, no swizzle, zero fill out of bounds (conv_multi_gemm.cu):
+// [outer][inner] elements, row stride stride_bytes, box [box_outer][box_inner]
+bool encode_f32_2d_plain(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                         uint32_t box_inner, uint32_t box_outer);
 
 // empty PDL-attributed kernel (the launch floor, diagnostics)
 cudaError_t launch_nop(cudaStream_t s);
