@@ -100,8 +100,12 @@ struct SimtShape {
     __device__ static int row(int tm, int i) { return tm + TMG * i; }     // interleaved thread rows
 };
 
-template <int BM, int BN, int TN, bool kTmaF>
-__global__ void __launch_bounds__(kSimtThreads, 2)
+// NST: ring stages (NST = 2: two CTAs per SM, 128 registers; NST >= 3: one
+// CTA per SM, up to 255 registers).  One barrier per chunk: right after it,
+// the stage chunk c - 1 used — which every thread has finished, as the
+// barrier guarantees — is refilled with chunk c + NST - 1.
+template <int BM, int BN, int TN, bool kTmaF, int NST>
+__global__ void __launch_bounds__(kSimtThreads, NST == 2 ? 2 : 1)
 kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ I, int C, int Wx, int Wy,
            const float *__restrict__ F,
            int K, int M, float *__restrict__ O, int ch_per_split, int CB, float *__restrict__ W, int dbg_in,
@@ -129,10 +133,10 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
     const int RS = kTmaF ? CKP : simt_rs(CKP);
 
     extern __shared__ __align__(128) float smem[];
-    float *Fst = smem;                              // [2][BM][RS]   F rows as stored (k fastest)
-    float *Bst = smem + 2 * BM * RS;                // [2][CKP][BN]  im2col tile
-    int *koff = reinterpret_cast<int *>(Bst + 2 * CKP * BN);   // [CKP]
-    uint64_t *fbar = reinterpret_cast<uint64_t *>(koff + ((CKP + 1) & ~1));   // [2] F stage barriers (TMA)
+    float *Fst = smem;                              // [NST][BM][RS]   F rows as stored (k fastest)
+    float *Bst = smem + NST * BM * RS;              // [NST][CKP][BN]  im2col tile
+    int *koff = reinterpret_cast<int *>(Bst + NST * CKP * BN);   // [CKP]
+    uint64_t *fbar = reinterpret_cast<uint64_t *>(koff + ((CKP + 1) & ~1));   // [NST] F stage barriers (TMA)
 
     const int S = gridDim.x;                        // split count (== cluster size when W == nullptr)
     const int split = blockIdx.x;
@@ -237,33 +241,40 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
 
     if (kTmaF && tid == 0) {
         tma_prefetch_desc(&tmapF);
-        mbar_init(&fbar[0], 1);
-        mbar_init(&fbar[1], 1);
+#pragma unroll
+        for (int j = 0; j < NST; ++j) mbar_init(&fbar[j], 1);
         fence_mbar_init();
     }
     pdl_wait();
     pdl_trigger();
     if (tl) g_simt_cta[5 * cta_lin + 1] = simt_gtimer();
     __syncthreads();                                // koff table, barriers
-    // two-stage ring: chunk c lives in stage c & 1; chunk c + 1 is in flight
-    // while chunk c computes (the paper's prefetch rounds)
-    if (nchunks > 0) { load_f(0, 0); load_b(0, 0); }
-    cp_async_commit();
-    if (nchunks > 1) { load_f(1, 1); load_b(1, 1); }
-    cp_async_commit();
+    // NST-stage ring: chunk c lives in stage c % NST; chunks c + 1 .. c + NST - 1
+    // are in flight while chunk c computes (the paper's prefetch rounds)
+#pragma unroll
+    for (int j = 0; j < NST - 1; ++j) {
+        if (j < nchunks) { load_f(j, j); load_b(j, j); }
+        cp_async_commit();
+    }
+    int st = 0;
     for (int chunk = 0; chunk < nchunks; ++chunk) {
-        const int st = chunk & 1;
-        cp_async_wait<1>();                         // chunk c staged (c + 1 may be in flight)
+        cp_async_wait<NST - 2>();                   // chunk c staged (newer ones may be in flight)
         __syncthreads();
-        if constexpr (kTmaF) mbar_wait(&fbar[st], (chunk >> 1) & 1);
+        if constexpr (kTmaF) mbar_wait(&fbar[st], (chunk / NST) & 1);
         if (tl && chunk == 0) g_simt_cta[5 * cta_lin + 2] = simt_gtimer();
+        {                                           // refill the stage chunk c - 1 used
+            const int nx = chunk + NST - 1;
+            const int sx = st == 0 ? NST - 1 : st - 1;
+            if (nx < nchunks) { load_f(nx, sx); load_b(nx, sx); }
+            cp_async_commit();
+        }
         // A = F rows in place: thread rows tm + i * TMG (consecutive rows across
         // the warp's lanes: conflict-free 16-B loads along k), four k per load;
         // B = the im2col tile, TN consecutive pixels per k
         const float *Fa = Fst + st * BM * RS + tm * RS;
         const float *Bs = Bst + st * CKP * BN + tn * 4;
         const float *Bs2 = Bst + st * CKP * BN + SH::R1 + tn * T2;
-#pragma unroll 1
+#pragma unroll(NST >= 3 ? 2 : 1)
         for (int kq = 0; kq < CKP; kq += 4) {
             float4 a[8];
 #pragma unroll
@@ -289,9 +300,7 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
                 }
             }
         }
-        __syncthreads();                            // every thread is done with stage st
-        if (chunk + 2 < nchunks) { load_f(chunk + 2, st); load_b(chunk + 2, st); }
-        cp_async_commit();
+        st = st + 1 == NST ? 0 : st + 1;
     }
     cp_async_wait<0>();
     if (tl) g_simt_cta[5 * cta_lin + 3] = simt_gtimer();
@@ -373,9 +382,9 @@ constexpr SimtTile kSimtTiles[kNumSimtTiles] = {
     {256, 48, 6}, {128, 96, 6}, {64, 192, 6},
     {256, 32, 4}, {128, 64, 4}, {64, 128, 4}};
 
-int simt_smem(int BM, int BN, int CK) {
+int simt_smem(int BM, int BN, int CK, int nst = 2) {
     const int CKP = (CK + 3) & ~3;
-    const int bytes = (2 * BM * simt_rs(CKP) + 2 * CKP * BN) * 4 + ((CKP + 1) & ~1) * 4 + 16;
+    const int bytes = (nst * BM * simt_rs(CKP) + nst * CKP * BN) * 4 + ((CKP + 1) & ~1) * 4 + 8 * nst;
     const int pbytes = BM * BN * 4;
     return bytes > pbytes ? bytes : pbytes;
 }
@@ -426,7 +435,7 @@ double sm_time(int n, int q, double w, int nch, int BM) {
     return n * (w / kEff1 + c);
 }
 
-struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; };
+struct SimtCfg { int tile, S, CB, cps, ws, smem; double t; int nst = 2; };
 
 SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, int Nimg) {
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
@@ -490,8 +499,17 @@ bool simt_forced(int C, int K, SimtCfg *c) {
 
 SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, int Nimg) {
     SimtCfg c;
-    if (simt_forced(C, K, &c) && (allow_ws || !c.ws)) return c;
-    return simt_choose(C, Wx, Wy, K, M, allow_ws, sd, Nimg);
+    if (!(simt_forced(C, K, &c) && (allow_ws || !c.ws))) c = simt_choose(C, Wx, Wy, K, M, allow_ws, sd, Nimg);
+    // ring depth (planner override B200CONV_SIMT_NST = 3 | 4: one CTA per SM)
+    if (c.tile >= 0) {
+        const int nst = env_override("B200CONV_SIMT_NST", c.nst);
+        const SimtTile &T = kSimtTiles[c.tile];
+        if (nst >= 3 && nst <= 4 && simt_smem(T.BM, T.BN, c.CB * K * K, nst) <= 227 * 1024) {
+            c.nst = nst;
+            c.smem = simt_smem(T.BM, T.BN, c.CB * K * K, nst);
+        }
+    }
+    return c;
 }
 
 int64_t out_px(int Wx, int Wy, int K, int sd) { return (int64_t)((Wy - K) / sd + 1) * ((Wx - K) / sd + 1); }
@@ -554,7 +572,10 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
         tma = encode_f32_2d_plain(&tmap, F, (uint64_t)C * K * K, (uint64_t)M, (uint64_t)C * K * K * 4, CK, BM);
     }
     if (!tma) memset(&tmap, 0, sizeof(tmap));
-    auto kern = tma ? kms_kernel<BM, BN, TN, true> : kms_kernel<BM, BN, TN, false>;
+    // the deeper one-CTA-per-SM rings exist for the TMA-fed variant only
+    auto kern = !tma ? kms_kernel<BM, BN, TN, false, 2>
+                     : c.nst == 3 ? kms_kernel<BM, BN, TN, true, 3>
+                     : c.nst == 4 ? kms_kernel<BM, BN, TN, true, 4> : kms_kernel<BM, BN, TN, true, 2>;
     cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -581,7 +602,7 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
 }
 
 int simt_max_clusters(int cluster, int smem) {
-    auto kern = kms_kernel<128, 128, 8, false>;
+    auto kern = kms_kernel<128, 128, 8, false, 2>;
     ensure_smem((const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster, 1, 1);
