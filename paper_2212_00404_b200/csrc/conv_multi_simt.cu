@@ -417,20 +417,21 @@ void simt_split(int C, int S, int BM, int BN, int K, int *CB, int *cps) {
 // / two resident CTAs; constants fitted (tools/simt_model.py) to a measured
 // sweep of every (tile, split, mode) on the bench layers (tools/simt_sweep.py,
 // B200): the planner's pick is within 1.5% of the best measured on average.
-// (Refit after the staging rewrite on sweep v3 (profiles/sweeps/): kEff1
-// 0.35, kEff2 0.50, TN = 6 / 4 penalty 0.9, and a per-chunk cost that scales
-// with BM (the F-row load and transpose of a chunk are BM x CK elements):
-// AlexNet 27.9 -> 25.9 us, target 30.5 -> 28.2, ResNet 14x14 13.5 -> 12.9.)
+// (Refit for the FFMA2 / TMA-ring kernel on the dense sweep v4
+// (profiles/sweeps/simt_sweep_v4_r02.log): kEff1 0.40, kEff2 0.45, TN = 6
+// weight 0.85, 0.8 us per chunk; the pick is the measured best on 7 of the 8
+// bench layers and within 1% on the eighth.)
 constexpr double kFmaPerUs = 128.0 * 1965.0;
-constexpr double kEff1 = 0.35, kEff2 = 0.50;
+constexpr double kEff1 = 0.40, kEff2 = 0.45;
 constexpr double kCtaFixed = 0.5;      // prologue (first chunk latency) + epilogue
-constexpr double kPerChunk = 0.4;      // per channel chunk of a BM = 128 tile: barriers, F transpose, load issue
+constexpr double kPerChunk = 0.8;      // per channel chunk: ring barrier, B gather issue, F TMA round trip
 constexpr double kClusterReduce = 9.0; // cluster co-scheduling + barrier waits + DSMEM reduction
 constexpr double kWsReduce = 0.5;      // second launch (PDL-overlapped) + its tail
 constexpr double kL2BytesPerUs = 3.0e6;
 
 double sm_time(int n, int q, double w, int nch, int BM) {
-    const double c = kCtaFixed + nch * kPerChunk * (BM / 128.0);
+    const double c = kCtaFixed + nch * kPerChunk;
+    (void)BM;
     if (q >= 2) return (n / 2) * (2.0 * w / kEff2) + (n % 2) * (w / kEff1) + ((n + 1) / 2) * c;
     return n * (w / kEff1 + c);
 }
@@ -447,7 +448,7 @@ SimtCfg simt_choose(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, 
         const int npt = (int)((px + T.BN - 1) / T.BN);
         const int nmt = (M + T.BM - 1) / T.BM;
         const int tiles = npt * nmt;
-        const double tn_pen = T.TN == 8 ? 1.0 : 0.9;                          // fitted per thread tile
+        const double tn_pen = T.TN == 6 ? 0.85 : 1.0;                         // fitted per thread tile
         int last_S = -1;
         for (int Sreq = 1; Sreq <= C && Sreq <= 96; ++Sreq) {
             int CB, cps;

@@ -22,7 +22,8 @@ def rs(ck):
 
 
 def smem(BM, BN, CK):
-    b = (CK * BM + 2 * CK * BN + BM * rs(CK)) * 4 + CK * 4
+    CKP = (CK + 3) & ~3                          # two-stage ring of F rows + im2col tile
+    b = (2 * BM * rs(CKP) + 2 * CKP * BN) * 4 + ((CKP + 1) & ~1) * 4 + 16
     return max(b, BM * BN * 4)
 
 
