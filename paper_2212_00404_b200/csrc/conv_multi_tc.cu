@@ -454,6 +454,12 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
             tc_fence_after();
         }
         if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 3] = tc_gtimer();
+        // the split-K partial tile P reuses the ring's smem: every gather warp's
+        // patch reads are ordered before it through the stage barriers and the
+        // MMA commit; this named barrier (the 8 gather / epilogue warps only)
+        // states that ordering explicitly (compute-sanitizer racecheck does not
+        // follow the tcgen05.commit chain)
+        if (S > 1) asm volatile("bar.sync 1, 256;" ::: "memory");
         constexpr int NCB = BN / 32;                     // 32-column blocks
         for (int cb = half; cb < NCB; cb += 2) {
             uint32_t r[32];

@@ -172,7 +172,7 @@ ks_kernel(const KsArgs a) {
     if constexpr (kPlain) {
     for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
         const int gi = idx / GS, e = idx - gi * GS;
-        const int f = e / KK, t = e - f * KK;
+        const int t = e / R, f = e - t * R;         // taps [t][f]: filter pairs adjacent (FFMA2)
         int g = g_first + gi;
         if (g >= NG) g -= NG;
         const int m = g * R + f;
@@ -199,7 +199,7 @@ ks_kernel(const KsArgs a) {
         // kC channels (f32 or bf16) -> f32 shared copies, plain loads
         for (int idx = tid; idx < ngr * GS; idx += kKsThreads) {
             const int gi = idx / GS, e = idx - gi * GS;
-            const int f = e / CKK, t = e - f * CKK;
+            const int t = e / R, f = e - t * R;     // taps [t][f]
             int g = g_first + gi;
             if (g >= NG) g -= NG;
             const int m = g * R + f;
@@ -301,11 +301,26 @@ ks_kernel(const KsArgs a) {
                     for (int q = 0; q < RR; ++q) {
                         const int r = ir - q;         // filter row feeding output row q
                         if (r >= 0 && r < K) {
+                            const int tap = (ch * KK + r * K + c) * R;
+                            // paired FMAs (FFMA2, ptx.cuh) along filter pairs
+                            // (broadcast input pixel; taps staged [t][f], so
+                            // a pair is one aligned register pair); bitwise the
+                            // same as fmaf.  (Pairing along pixels needs the
+                            // odd-c window pairs re-formed by moves: measured
+                            // slower on K = 5 / 7, R = 1, so those stay FFMA.)
+                            if constexpr (R % 2 == 0) {
 #pragma unroll
-                            for (int f = 0; f < R; ++f)
+                                for (int f = 0; f < R; f += 2)
 #pragma unroll
-                                for (int v = 0; v < TX; ++v)
-                                    acc[q][f][v] = fmaf(win[v + c], w[f * CKK + ch * KK + r * K + c], acc[q][f][v]);
+                                    for (int v = 0; v < TX; ++v)
+                                        ffma2(acc[q][f][v], acc[q][f + 1][v], win[v + c], w[tap + f], w[tap + f + 1]);
+                            } else {
+#pragma unroll
+                                for (int f = 0; f < R; ++f)
+#pragma unroll
+                                    for (int v = 0; v < TX; ++v)
+                                        acc[q][f][v] = fmaf(win[v + c], w[tap + f], acc[q][f][v]);
+                            }
                         }
                     }
             }
