@@ -1,28 +1,31 @@
 #!/bin/bash
-# Round profile capture (run under gpurun from the repo root):
-#   1. ncu launch list of one bench step (kernel durations, cold, serialised)
-#   2. per-launch DRAM traffic of every hot-path kernel of one step
-#   3. one --set full capture of the dominant kernel's heaviest launch
+# Round profile capture (run under gpurun from the repo root): tools/profile_round.sh <tag>
+#   1. ncu launch list of the headline step (configs[4] x FP32/TF32/BF16; cold, serialised)
+#   2. --set full captures: KM-SIMT (configs[4] FP32), KM-TC/G GEMM (configs[4] TF32, BF16),
+#      KM-TC implicit (28x28x256 N=1 TF32, BF16), KS (224x224 K=3 M=256)
+#   3. KS DRAM-write evidence: 12 launches of 224x224 K=1 M=256 writing rotating O buffers,
+#      --cache-control none (a launch's write-back lands partly in later launches: the
+#      per-launch average over the sequence is the DRAM traffic of one launch)
 set -u
-R=${1:-r01}
+R=${1:-r02}
 mkdir -p gpurun_out
-BENCH="python bench.py --steps 2 --warmup 1 --cudnn 0 --cpu-seconds 0 --layers 0 --e2e-steps 1"
 K='regex:ks_kernel|kms_kernel|kmtc_kernel|kmtc_persist_kernel|kmn_kernel|splitk_reduce|im2col_kernel|gemm_kernel|pad_kernel|pad_rows_kernel'
-NL=$(python -c "import bench; from paper_2212_00404_b200 import conv; print(sum((conv.plan_single(c['Wx'],c['Wy'],c['K'],c['M']) if c['kind']=='single' else conv.plan_multi(c['C'],c['Wx'],c['Wy'],c['K'],c['M'],c['prec']))['launches'] for c in bench.suite()))")
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-    --clock-control none -k "$K" -c $NL --csv --log-file gpurun_out/launches_$R.csv $BENCH \
-    > gpurun_out/launches_$R.log 2>&1
+    --clock-control none -k "$K" -c 12 --csv --log-file gpurun_out/launches_$R.csv \
+    python bench.py --steps 3 --warmup 3 --suite 0 --e2e 0 --cpu-seconds 0 > /dev/null 2>&1
 echo "launches rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:kms_kernel -s 2 -c 1 \
-    -o gpurun_out/full_simt_$R python tools/run_layer.py sweep_14x14_c512_m4096_k3:fp32 3 \
-    > /dev/null 2>&1
-echo "full rc=$?"
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:ks_kernel -s 2 -c 1 \
-    -o gpurun_out/full_ks_$R python tools/run_layer.py single_224x224_k1_m256:fp32 3 > /dev/null 2>&1
-echo "full ks rc=$?"
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 \
-    -o gpurun_out/full_tcg_$R python tools/run_layer.py sweep_14x14_c512_m4096_k3:bf16 3 > /dev/null 2>&1
-echo "full tcg rc=$?"
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:kmtc_persist_kernel -s 2 -c 1 \
-    -o gpurun_out/full_tcbatched_$R python tools/run_batched.py 64 tf32 3 > /dev/null 2>&1
-echo "full tc batched rc=$?"
+full() {  # full <name> <kernel regex> <layer label> [reps]
+  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$2" -s 2 -c 1 \
+      -o gpurun_out/full_$1_$R python tools/run_layer.py "$3" ${4:-3} > /dev/null 2>&1
+  echo "full $1 rc=$?"
+}
+full simt kms_kernel sweep_14x14_c512_m4096_k3:fp32
+full tcg_tf32 gemm_kernel sweep_14x14_c512_m4096_k3:tf32
+full tcg_bf16 gemm_kernel sweep_14x14_c512_m4096_k3:bf16
+full tc_tf32 kmtc_kernel target_28x28_c256_m256_k3:tf32 4
+full tc_bf16 kmtc_kernel target_28x28_c256_m256_k3:bf16 4
+full ks3 ks_kernel single_224x224_k3_m256:fp32 4
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_write.sum,dram__bytes_read.sum --cache-control none \
+    --clock-control none -k regex:ks_kernel --csv --log-file gpurun_out/ks_dram_seq_$R.csv \
+    python tools/run_layer.py single_224x224_k1_m256:fp32 12 > /dev/null 2>&1
+echo "ks dram seq rc=$?"
