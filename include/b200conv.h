@@ -62,6 +62,9 @@
  *   B200CONV_SIMT_FORCE=t,S,ws  KM-SIMT thread tile t, channel split S, ws=1:
  *                           reduced through the workspace
  *   B200CONV_C3=0           no KS-C3 (C = 3 stems take the general kernels)
+ *   B200CONV_PLANNER=paper  KS row blocks by the paper's N_FMA rule instead
+ *                           of the measured row threshold (NEXT-4 A/B)
+ *   B200CONV_SIMT_NST=2..4  KM-SIMT ring depth (3, 4: one CTA per SM)
  * Timeline stamps and work-skipping diagnostics exist only in the separate
  * -DB200CONV_DIAG build (libb200conv_diag.so), never in this library.
  *
@@ -226,6 +229,18 @@ B200CONV_API int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, in
  * over all N images; stride 1: conv_plan_multi_batched of the padded map). */
 B200CONV_API int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride,
                             int precision, conv_plan *out);
+
+/* The paper's latency-hiding model (§2.2; SURVEY §8(f)
+ * NEXT-4) for a device profile: profile 0 = the current B200 (577-clock DRAM
+ * latency, 128 FP32 lanes and the measured 6554 GB/s at 1965 MHz), 1 = the
+ * paper's GTX 1080Ti (Table 1).  out[5] receives N_FMA (FMAs per
+ * SM per data set for method 1), the latency volume (bytes per clock x
+ * latency), the 4-B loading threads per SM that move it (rounded up to the
+ * core count), V_s (the minimum volume they move) and bytes per clock.
+ * CONV_E_NULL / CONV_E_SHAPE (unknown profile) on bad arguments.  The KM-SIMT
+ * planner sets its ring depth from it; the KS planner does with
+ * B200CONV_PLANNER=paper. */
+B200CONV_API int conv_latency_model(int profile, double *out);
 
 B200CONV_API const char *conv_status_string(int status);
 

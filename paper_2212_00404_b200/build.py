@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libb200conv.so")
 SOURCES = ["abi.cu", "conv_single.cu", "conv_multi_simt.cu", "conv_multi_tc.cu", "conv_multi_gemm.cu", "workspace.cu"]
-HEADERS = ["kernels.h", "ptx.cuh"]
+HEADERS = ["kernels.h", "ptx.cuh", "latency_model.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -30,7 +30,7 @@ EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv
            "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_multi_batched_ex",
            "conv_plan_multi_batched", "conv_single_pad_ex", "conv_multi_pad_ex",
            "conv_single_strided_ex", "conv_multi_strided_ex", "conv_plan_multi_strided", "conv_plan_single", "conv_plan_multi", "conv_status_string",
-           "conv_version"]
+           "conv_version", "conv_latency_model"]
 
 
 class ConvError(RuntimeError):
@@ -85,6 +85,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
             lib.conv_status_string.argtypes = [I32]
             lib.conv_status_string.restype = ctypes.c_char_p
             lib.conv_version.argtypes = []
+            lib.conv_latency_model.argtypes = [I32, ctypes.POINTER(ctypes.c_double)]
             lib.conv_diag_nop.argtypes = [P]
             lib.conv_diag_nop.restype = I32
             for n in EXPORTS:
@@ -187,6 +188,14 @@ def plan_multi(C, Wx, Wy, K, M, precision="fp32") -> dict:
     p = ConvPlan()
     _check(load().conv_plan_multi(C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
     return p.as_dict()
+
+
+def latency_model(profile: str = "b200") -> dict:
+    """The paper's latency-hiding model (§2.2) for "b200" (this
+    device) or "gtx1080ti" (the paper's Table 1)."""
+    out = (ctypes.c_double * 5)()
+    _check(load().conv_latency_model({"b200": 0, "gtx1080ti": 1}[profile], out))
+    return dict(zip(("n_fma", "volume", "threads_per_sm", "v_s", "bytes_per_clk"), list(out)))
 
 
 def diag_nop(stream=None):

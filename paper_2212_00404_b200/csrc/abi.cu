@@ -12,10 +12,16 @@
 #include <utility>
 #include <cuda_runtime.h>
 #include "kernels.h"
+#include "latency_model.h"
 
 using namespace b200;
 
 int b200::pdl_enabled() { return env_override("B200CONV_PDL", 1) != 0; }
+
+bool b200::planner_paper_model() {
+    const char *e = getenv("B200CONV_PLANNER");
+    return e && e[0] == 'p';
+}
 
 int b200::env_override(const char *name, int def) {
     const char *e = getenv(name);
@@ -545,6 +551,19 @@ int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad,
             return plan_multi_gemm(C, Wxp, Wyp, K, M, precision == CONV_BF16, out, stride, N) ? CONV_E_SHAPE : CONV_OK;
         default: return CONV_E_PRECISION;
     }
+}
+
+int conv_latency_model(int profile, double *out) {
+    if (!out) return CONV_E_NULL;
+    if (profile != 0 && profile != 1) return CONV_E_SHAPE;
+    const DeviceProfile d = profile == 1 ? kGtx1080Ti : b200_profile(num_sms());
+    const LatencyModel m = latency_model(d);
+    out[0] = m.n_fma;
+    out[1] = m.volume;
+    out[2] = m.threads_per_sm;
+    out[3] = m.v_s;
+    out[4] = d.bytes_per_clk;
+    return CONV_OK;
 }
 
 const char *conv_status_string(int status) {

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include "kernels.h"
+#include "latency_model.h"
 #include "ptx.cuh"
 
 namespace b200 {
@@ -501,10 +502,24 @@ bool simt_forced(int C, int K, SimtCfg *c) {
 SimtCfg simt_config(int C, int Wx, int Wy, int K, int M, bool allow_ws, int sd, int Nimg) {
     SimtCfg c;
     if (!(simt_forced(C, K, &c) && (allow_ws || !c.ws))) c = simt_choose(C, Wx, Wy, K, M, allow_ws, sd, Nimg);
-    // ring depth (planner override B200CONV_SIMT_NST = 3 | 4: one CTA per SM)
+    // ring depth.  The paper's model (§2.2, NEXT-4): a chunk carries
+    // q x BM x BN x CK FMAs per SM; at or above N_FMA (method 1) one chunk
+    // in flight behind the one computing hides the latency: two stages, two
+    // CTAs per SM.  Below it (method 2) the deepest ring that fits keeps the
+    // most bytes in flight (one CTA per SM).  Measured: every bench layer is
+    // method 1, and 3 / 4 stages are 1-10 % slower.
+    // Planner override B200CONV_SIMT_NST = 2..4.
     if (c.tile >= 0) {
-        const int nst = env_override("B200CONV_SIMT_NST", c.nst);
         const SimtTile &T = kSimtTiles[c.tile];
+        int nst_model = 2;
+        {
+            const LatencyModel lm = latency_model(b200_profile(num_sms()));
+            const int q = c.smem <= 113 * 1024 ? 2 : 1;
+            const double fma_chunk = (double)q * T.BM * T.BN * c.CB * K * K;
+            if (paper_method(lm, fma_chunk) == 2)
+                nst_model = simt_smem(T.BM, T.BN, c.CB * K * K, 4) <= 227 * 1024 ? 4 : 3;
+        }
+        const int nst = env_override("B200CONV_SIMT_NST", nst_model);
         if (nst >= 3 && nst <= 4 && simt_smem(T.BM, T.BN, c.CB * K * K, nst) <= 227 * 1024) {
             c.nst = nst;
             c.smem = simt_smem(T.BM, T.BN, c.CB * K * K, nst);

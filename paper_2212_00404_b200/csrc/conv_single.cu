@@ -29,6 +29,7 @@
 #include <type_traits>
 #include <cuda_bf16.h>
 #include "kernels.h"
+#include "latency_model.h"
 #include "ptx.cuh"
 
 namespace b200 {
@@ -451,7 +452,17 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
     // 2.0 us, 28x28 K=3 2.24 -> 2.05 us; K >= 5 at 28x28 and K = 3 at 56x56
     // get slower).  B200CONV_KS_SMALL=<max Ho> overrides (0: off).
     const int small_ho = kDiag ? env_override("B200CONV_KS_SMALL", K == 3 ? 32 : 16) : (K == 3 ? 32 : 16);
-    const bool small = K >= 3 && Ho <= small_ho;
+    bool small = K >= 3 && Ho <= small_ho;
+    if (planner_paper_model() && K >= 3) {
+        // the paper's procedure (§2.2; NEXT-4): each SM's data set
+        // is its share of the layer (the band a CTA stages, all filters);
+        // fewer than N_FMA FMAs per SM -> method 2 (volume / latency bound):
+        // 1-row blocks, the most independent units in flight; else method 1:
+        // register row blocks, more FMAs per staged byte
+        const LatencyModel lm = latency_model(b200_profile(num_sms()));
+        const double fma_per_sm = (double)M * Ho * Wo * K * K / num_sms();
+        small = paper_method(lm, fma_per_sm) == 2;
+    }
     const int TX = ks_TX(K), R = kC > 1 ? ks_R_c3(K) : ks_R(K), RR = small ? 1 : ks_RR(K);
     KsArgs a = {};
     a.I = I; a.F = F; a.O = O;

@@ -24,6 +24,13 @@ constexpr bool kDiag = true;
 constexpr bool kDiag = false;
 #endif
 
+// NEXT-4: B200CONV_PLANNER=paper makes the KS row-block decision follow the
+// paper's latency model (§2.2 procedure) instead of the measured
+// threshold; A/B in profiles/planner_ab_r02.txt (the model is 4 % slower over
+// the 17 layers where the two differ, so the threshold is the default).  The
+// KM-SIMT ring depth always follows the model (its choice is the measured best).
+bool planner_paper_model();
+
 // Documented planner overrides (include/b200conv.h "Planner overrides"): an
 // integer environment variable, or `def` when unset.  They only choose among
 // correct plans (tests force every path with them); read at each call.

@@ -22,7 +22,7 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 19
+    assert len(syms) == 20
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
@@ -204,3 +204,21 @@ def test_verify_cli_usage_and_infeasible_exit_codes():
     assert run("--mode", "single", "--wx", "8", "--wy", "8", "--k", "3", "--m", "2", "--c", "3") == 1
     assert run("--mode", "multi", "--wx", "4", "--wy", "4", "--c", "2", "--k", "5", "--m", "2") == 2
     assert run("--help") == 0
+
+
+def test_latency_model_reproduces_the_papers_table1_numbers():
+    """PAPER.md §2.2: GTX 1080Ti, 258-clock latency, 128 cores x 2
+    FMA per clock -> N_FMA = 66,048; 327 B/clk x 258 = 84,366 bytes; 768
+    threads per SM fetching one 4-B word; V_s = 768 x 4 x 28 = 86,016."""
+    m = conv.latency_model("gtx1080ti")
+    assert m["n_fma"] == 66048 and m["volume"] == 84366
+    assert m["threads_per_sm"] == 768 and m["v_s"] == 86016 and m["bytes_per_clk"] == 327
+
+
+def test_latency_model_b200_profile():
+    m = conv.latency_model("b200")
+    assert m["n_fma"] == 577 * 128                        # 1 FMA per lane per clock (reading Q15)
+    assert abs(m["bytes_per_clk"] - 6554e9 / 1965e6) < 1e-6
+    assert m["threads_per_sm"] % 128 == 0 and m["v_s"] >= m["volume"]
+    assert conv.load().conv_latency_model(7, (ctypes.c_double * 5)()) == 1        # unknown profile
+    assert conv.load().conv_latency_model(0, None) == 2                           # null
