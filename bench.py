@@ -407,7 +407,53 @@ def _strong_extras(args, conv, dev, stream, world, rank, c, bufs, Ml, byp):
         t1 = float(t1b.item())
         res[p] = {"t1_us": round(t1, 2), "tN_us": byp[p]["us"], "speedup": round(t1 / byp[p]["us"], 2),
                   "allgather_us": round(ag, 2), "allgather_recv_bytes": int(4 * (M - Ml) * Ho * Wo)}
+        res[p].update(_fused_allgather(conv, dev, stream, world, rank, c, bufs[p], Ml, p, reps))
     return res
+
+
+_SYMM = {}
+
+
+def _fused_allgather(conv, dev, stream, world, rank, c, buf, Ml, prec, reps):
+    """NEXT-2: conv with the all-gather fused into the epilogue
+    (conv_multi_allgather_ex) into a torch symmetric-memory O: every rank's
+    kernels store their rows straight into all ranks' O over NVLink (one
+    multimem.st per value when the NVSwitch multicast object exists).  Device
+    time per call, max over ranks; the barrier that publishes the rows is
+    timed with it."""
+    import torch
+    import torch.distributed as dist
+    try:
+        import torch.distributed._symmetric_memory as symm
+        C, Wx, Wy, K, M, Ho, Wo = (c[k] for k in ("C", "Wx", "Wy", "K", "M", "Ho", "Wo"))
+        if "O" not in _SYMM:
+            O = symm.empty((M, Ho, Wo), dtype=torch.float32, device=dev)
+            hdl = symm.rendezvous(O, dist.group.WORLD)
+            off = O.data_ptr() - hdl.buffer_ptrs[rank]
+            peers = [hdl.buffer_ptrs[(rank + r) % world] + off for r in range(world)]
+            mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+            _SYMM.update(O=O, hdl=hdl, peers=peers, mc=(mc + off) if mc else None)
+        I, Fs, _ = buf
+        m0 = rank * Ml
+
+        def call():
+            conv.conv_multi_allgather_ex(I, C, Wx, Wy, Fs[0], K, Ml, m0, M, _SYMM["peers"], _SYMM["mc"], prec,
+                                         stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                call()
+            stream.synchronize()
+            dist.barrier()
+            a, b = _ev(), _ev()
+            a.record(stream)
+            for _ in range(reps):
+                call()
+            b.record(stream)
+            stream.synchronize()
+        us = _max_over_ranks([1e3 * a.elapsed_time(b) / reps], dev, world)[0]
+        return {"fused_allgather_us": round(us, 2), "fused_path": "multimem" if _SYMM["mc"] else "peer stores"}
+    except Exception as exc:                       # reported, never fatal for the bench line
+        return {"fused_allgather_error": repr(exc)[:120]}
 
 
 def _traffic_lookup(kernel, world):
@@ -822,7 +868,9 @@ def run_ours(args):
                                              "multi_tf32", "multi_bf16")} if suite_res else None),
     }
     if "sweep_strong" in hl:
-        res["sweep_strong"] = hl["sweep_strong"]
+        detail["sweep_strong"] = hl["sweep_strong"]
+        keep = ("t1_us", "tN_us", "speedup", "allgather_us", "fused_allgather_us")
+        res["sweep_strong"] = {p: {k: v[k] for k in keep if k in v} for p, v in hl["sweep_strong"].items()}
     detail["suite"] = suite_res
     detail["clocks"] = clocks
     detail["paper_context"] = {"single_vs_cudnn71_avg": 2.6, "multi_vs_cudnn71_avg": 1.39,

@@ -230,6 +230,26 @@ B200CONV_API int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, in
 B200CONV_API int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride,
                             int precision, conv_plan *out);
 
+/* Filter-sharded call with the all-gather fused into the epilogue (SURVEY
+ * §8(f) NEXT-2; Fig. 2(c), lifted to GPUs): this rank's
+ * F [M][C][K][K] (filters m0 .. m0+M-1 of M_total) produces O rows
+ * [m0, m0+M) of the full O [M_total][Ho][Wo], and the final stores of the
+ * kernels write them straight into every rank's copy of O: O_peers[0..n_peers)
+ * are device pointers valid in this process (the local O and the peers' O
+ * mapped over NVLink, e.g. torch symmetric-memory buffer_ptrs), n_peers <= 8.
+ * O_mc, when non-null, is a multicast address of that buffer (NVSwitch
+ * multicast object, e.g. symmetric-memory multicast_ptr): every value is then
+ * ONE multimem.st reaching all GPUs, and O_peers[0] is still required.  The
+ * final-store sites of the KM-SIMT split-K reduce and of the KM-TC/G GEMM are
+ * peer-aware; other plans (implicit KM-TC, KS-C3, unsplit KM-SIMT) store
+ * locally and a copy kernel in the same stream pushes the rows to the peers.
+ * The data is complete on a rank once every rank's call has finished (e.g.
+ * stream sync + a process-group barrier).  Errors as conv_multi_ex, plus
+ * CONV_E_SHAPE for m0 < 0, m0 + M > M_total, n_peers outside 1..8. */
+B200CONV_API int conv_multi_allgather_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, int m0,
+                                         int M_total, float *const *O_peers, int n_peers, float *O_mc, int precision,
+                                         void *stream);
+
 /* The paper's latency-hiding model (§2.2; SURVEY §8(f)
  * NEXT-4) for a device profile: profile 0 = the current B200 (577-clock DRAM
  * latency, 128 FP32 lanes and the measured 6554 GB/s at 1965 MHz), 1 = the

@@ -30,7 +30,7 @@ EXPORTS = ["conv_single", "conv_multi", "conv_single_ex", "conv_multi_ex", "conv
            "conv_multi_host", "conv_single_host_async", "conv_multi_host_async", "conv_multi_batched_ex",
            "conv_plan_multi_batched", "conv_single_pad_ex", "conv_multi_pad_ex",
            "conv_single_strided_ex", "conv_multi_strided_ex", "conv_plan_multi_strided", "conv_plan_single", "conv_plan_multi", "conv_status_string",
-           "conv_version", "conv_latency_model"]
+           "conv_version", "conv_latency_model", "conv_multi_allgather_ex"]
 
 
 class ConvError(RuntimeError):
@@ -86,6 +86,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
             lib.conv_status_string.restype = ctypes.c_char_p
             lib.conv_version.argtypes = []
             lib.conv_latency_model.argtypes = [I32, ctypes.POINTER(ctypes.c_double)]
+            lib.conv_multi_allgather_ex.argtypes = [P, I32, I32, I32, P, I32, I32, I32, I32,
+                                                    ctypes.POINTER(ctypes.c_void_p), I32, P, I32, P]
             lib.conv_diag_nop.argtypes = [P]
             lib.conv_diag_nop.restype = I32
             for n in EXPORTS:
@@ -188,6 +190,15 @@ def plan_multi(C, Wx, Wy, K, M, precision="fp32") -> dict:
     p = ConvPlan()
     _check(load().conv_plan_multi(C, Wx, Wy, K, M, _prec(precision), ctypes.byref(p)))
     return p.as_dict()
+
+
+def conv_multi_allgather_ex(I, C, Wx, Wy, F, K, M, m0, M_total, O_peers, O_mc=None, precision="fp32",
+                            stream=None):
+    """NEXT-2: this rank's filters m0..m0+M-1 straight into every O in O_peers
+    (device pointers or tensors [M_total][Ho][Wo]); O_mc: multicast address."""
+    arr = (ctypes.c_void_p * len(O_peers))(*[_ptr(o) for o in O_peers])
+    _check(load().conv_multi_allgather_ex(_ptr(I), C, Wx, Wy, _ptr(F), K, M, m0, M_total, arr, len(O_peers),
+                                          _ptr(O_mc), _prec(precision), _stream(stream)))
 
 
 def latency_model(profile: str = "b200") -> dict:

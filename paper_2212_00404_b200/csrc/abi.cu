@@ -553,6 +553,51 @@ int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad,
     }
 }
 
+int conv_multi_allgather_ex(const void *I, int C, int Wx, int Wy, const void *F, int K, int M, int m0, int M_total,
+                            float *const *O_peers, int n_peers, float *O_mc, int precision, void *stream) {
+    CallScope scope;
+    int st = check_shape(C, Wx, Wy, K, M_total);
+    if (st) return st;
+    if (M < 1 || m0 < 0 || (int64_t)m0 + M > M_total || n_peers < 1 || n_peers > kMaxPeers) return CONV_E_SHAPE;
+    if (precision < CONV_FP32 || precision > CONV_BF16) return CONV_E_PRECISION;
+    if (!O_peers) return CONV_E_NULL;
+    for (int r = 0; r < n_peers; ++r)
+        if ((st = check_ptrs(I, F, O_peers[r], precision == CONV_BF16 ? 2 : 4))) return st;
+    if (O_mc && !aligned(O_mc, 4)) return CONV_E_ALIGN;
+    if ((st = check_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t plane = (int64_t)(Wy - K + 1) * (Wx - K + 1);
+    const int64_t off = (int64_t)m0 * plane;
+    float *O0 = O_peers[0] + off;
+    PeerOut po = {};
+    for (int r = 1; r < n_peers; ++r) po.p[r - 1] = O_peers[r] + off;
+    po.n = n_peers - 1;
+    po.mc = O_mc ? O_mc + off : nullptr;
+    struct Reset { ~Reset() { set_peer_out(nullptr); } } reset;
+    cudaError_t e;
+    if (c3_layer(C, Wx, Wy, K, M)) {            // KS-C3: plain stores, then the peer copy
+        set_peer_out(nullptr);
+        e = launch_multi_c3(I, C, Wx, Wy, F, K, M, O0, precision == CONV_BF16, s);
+        set_peer_out(&po);
+        if (e == cudaSuccess) e = launch_peer_copy(O0, M * plane, s);
+    } else if (precision == CONV_FP32) {        // split-K reduce stores to every peer (else a copy)
+        set_peer_out(&po);
+        e = launch_multi_simt(static_cast<const float *>(I), C, Wx, Wy, static_cast<const float *>(F), K, M, O0, s);
+    } else {                                    // KM-TC/G epilogue stores to every peer
+        const bool bf16 = precision == CONV_BF16;
+        set_peer_out(&po);
+        e = launch_multi_gemm(I, C, Wx, Wy, F, K, M, O0, bf16, s);
+        if (e == cudaErrorNotSupported) {       // implicit kernel: plain stores, then the peer copy
+            cudaGetLastError();
+            set_peer_out(nullptr);
+            e = launch_multi_tc(I, C, Wx, Wy, F, K, M, O0, bf16, s);
+            set_peer_out(&po);
+            if (e == cudaSuccess) e = launch_peer_copy(O0, M * plane, s);
+        }
+    }
+    return launch_status(e);
+}
+
 int conv_latency_model(int profile, double *out) {
     if (!out) return CONV_E_NULL;
     if (profile != 0 && profile != 1) return CONV_E_SHAPE;

@@ -93,6 +93,7 @@ struct GmArgs {
     int stages, stage_bytes;
     float *O;
     float *Wk;        // split-K partials [S][tiles][BN][128] (nullptr: DSMEM reduction)
+    PeerOut po;       // NEXT-2: extra / multicast destinations of every O store
 };
 
 template <bool kTF32, int BN, bool kModeF>
@@ -211,15 +212,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             const int x = p - y * g.Wx, n = y / g.Ho;
                             y -= n * g.Ho;
                             if (n < g.N && x < g.Wo)
-                                g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = __uint_as_float(r[j]);
+                                out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, __uint_as_float(r[j]));
                         }
                     } else if (m < g.M) {
                         const int p = b0 + cb * 32;
                         int y = p / g.Wx, x = p - y * g.Wx;
-                        float *orow = g.O + (int64_t)m * plane;
+                        const int64_t orow = (int64_t)m * plane;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            if (y < g.Ho && x < g.Wo) orow[y * g.Wo + x] = __uint_as_float(r[j]);
+                            if (y < g.Ho && x < g.Wo) out_store(g.po, g.O, orow + y * g.Wo + x, __uint_as_float(r[j]));
                             if (++x == g.Wx) { x = 0; ++y; }
                         }
                     }
@@ -230,11 +231,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     const int x = p - y * g.Wx, n = y / g.Ho;      // n = image (0 unless batched)
                     y -= n * g.Ho;
                     if (n < g.N && x < g.Wo) {
-                        float *o = g.O + (int64_t)n * g.M * plane + (int64_t)y * g.Wo + x;
+                        const int64_t o = (int64_t)n * g.M * plane + (int64_t)y * g.Wo + x;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int m = b0 + cb * 32 + j;
-                            if (m < g.M) o[(int64_t)m * plane] = __uint_as_float(r[j]);
+                            if (m < g.M) out_store(g.po, g.O, o + (int64_t)m * plane, __uint_as_float(r[j]));
                         }
                     }
                 }
@@ -298,7 +299,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int m = a0 + row0 + e;
-                        if (m < g.M) g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = vv[e];
+                        if (m < g.M) out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, vv[e]);
                     }
                 }
             } else {
@@ -311,7 +312,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         int y = p / g.Wx;
                         const int x = p - y * g.Wx, n = y / g.Ho;
                         y -= n * g.Ho;
-                        if (n < g.N && x < g.Wo) g.O[((int64_t)n * g.M + m) * plane + y * g.Wo + x] = vv[e];
+                        if (n < g.N && x < g.Wo) out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, vv[e]);
                     }
                 }
             }
@@ -552,6 +553,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
         if (e != cudaSuccess) return e;
     }
     GmArgs g;
+    g.po = N == 1 ? peer_out() : PeerOut{};
     g.nkb = p.nkb;
     g.kbps = p.kbps;
     g.M = M;

@@ -610,7 +610,11 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     cfg.numAttrs = W ? 1 : 2;
     const int dbg = kDiag ? env_override("B200CONV_SIMT_DBG", 0) : 0;
     e = cudaLaunchKernelEx(&cfg, kern, tmap, I, C, Wx, Wy, F, K, M, O, c.cps, c.CB, W, dbg, sd, Nimg);
-    if (e != cudaSuccess || !W) return e;
+    if (e != cudaSuccess) return e;
+    if (!W) {                                   // (NEXT-2 peers: this epilogue is not peer-aware)
+        const PeerOut &po = peer_out();
+        return (po.n || po.mc) ? launch_peer_copy(O, (int64_t)M * out_px(Wx, Wy, K, sd) * Nimg, s) : e;
+    }
     const int ldw = p.grid_y * BN;
     const int64_t slice = (int64_t)p.grid_z * BM * ldw;
     const int plane = (int)out_px(Wx, Wy, K, sd);
@@ -646,7 +650,9 @@ cudaError_t launch_multi_simt(const float *I, int C, int Wx, int Wy, const float
         for (int n = 0; n < Nimg; ++n)
             kmn_kernel<<<p.grid_x, p.block_x, 0, s>>>(I + (int64_t)n * C * Wx * Wy, C, Wx, Wy, F, K, M,
                                                       O + n * out_img, sd);
-        return cudaGetLastError();
+        const PeerOut &po = peer_out();
+        if (cudaGetLastError() != cudaSuccess) return cudaErrorLaunchFailure;
+        return (po.n || po.mc) ? launch_peer_copy(O, out_img * Nimg, s) : cudaSuccess;
     }
     float *W = nullptr;
     if (c.ws) {

@@ -88,6 +88,33 @@ int choose_split(int tiles, int units, int max_split, int ctas_per_sm, float t_u
 // co-resident clusters of size S (1..16) for 1 or 2 CTAs per SM (same table)
 int clusters_resident(int S, int ctas_per_sm);
 
+// NEXT-2 (epilogue-fused all-gather of the filter-sharded O): the final-store
+// sites of the split-K reduce kernel and of the KM-TC/G GEMM write every
+// output value to the primary O and to up to kMaxPeers - 1 more buffers (peer
+// memory mapped into this process, e.g. torch symmetric memory), or ONE
+// multimem store to a multicast address covering all of them.  n == 0 and
+// mc == nullptr: a plain call.  Set by conv_multi_allgather_ex for the
+// duration of its launches (thread-local), read by those launchers.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+    float *p[kMaxPeers - 1];   // extra destinations, each offset like the primary O
+    float *mc;                 // multicast address of the primary O (replaces every store)
+    int n;                     // number of extra destinations
+};
+const PeerOut &peer_out();
+void set_peer_out(const PeerOut *po);       // nullptr: back to plain calls
+__device__ __forceinline__ void out_store(const PeerOut &po, float *O, int64_t idx, float v) {
+    if (po.mc) {
+        asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(po.mc + idx), "f"(v) : "memory");
+        return;
+    }
+    O[idx] = v;
+    for (int r = 0; r < po.n; ++r) po.p[r][idx] = v;
+}
+// copy n floats from src to every peer destination (fallback for plans whose
+// final stores are not peer-aware)
+cudaError_t launch_peer_copy(const float *src, int64_t n, cudaStream_t s);
+
 // Every ABI entry point holds a CallScope for the duration of the call: the
 // graph-private scratch allocated while a stream is being captured is freed
 // (cudaFreeAsync, in stream order) when the outermost scope ends.

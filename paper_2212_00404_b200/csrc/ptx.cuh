@@ -309,6 +309,12 @@ __device__ __forceinline__ void ffma2(float &d0, float &d1, float a, float b0, f
     asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
 }
 
+// One store to a multicast address: NVSwitch writes it to every GPU's memory
+// bound to the multicast object (PTX multimem.st, sm_90+).
+__device__ __forceinline__ void multimem_st_f32(float *mc, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

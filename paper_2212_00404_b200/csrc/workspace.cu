@@ -44,6 +44,12 @@ thread_local std::vector<std::pair<void *, cudaStream_t>> t_graph_scratch;
 thread_local int t_call_depth = 0;
 }  // namespace
 
+namespace {
+thread_local PeerOut t_peer_out = {};
+}
+const PeerOut &peer_out() { return t_peer_out; }
+void set_peer_out(const PeerOut *po) { t_peer_out = po ? *po : PeerOut{}; }
+
 CallScope::CallScope() { ++t_call_depth; }
 CallScope::~CallScope() {
     if (--t_call_depth > 0) return;
@@ -105,7 +111,7 @@ static void *buffer_get(std::map<std::pair<int, cudaStream_t>, WsBuf> &pool, siz
 template <int kRedG, bool kBatch>
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, int ldw, int N,
-                     float *__restrict__ O, int plane) {
+                     float *__restrict__ O, int plane, const PeerOut po) {
     pdl_wait();
     pdl_trigger();
     // 32-bit indexing: M * N <= INT_MAX is an ABI precondition
@@ -144,10 +150,10 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
         if (valid && g == 0) {
             const float v[4] = {a.x, a.y, a.z, a.w};
             if constexpr (!kBatch) {
-                float *o = O + (int64_t)m * N + n;
+                const int64_t o = (int64_t)m * N + n;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (n + i < N) o[i] = v[i];
+                    if (n + i < N) out_store(po, O, o + i, v[i]);
             } else {
                 // batch of N / plane images: column n + i is pixel (n+i) % plane of image (n+i) / plane
 #pragma unroll
@@ -237,6 +243,7 @@ cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, vo
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,
                                  cudaStream_t s, int plane) {
     if (plane <= 0) plane = N;
+    const PeerOut po = plane == N ? peer_out() : PeerOut{};
     // few splits: one lane per float4 of outputs; many: 8 lanes (latency)
     const int Gd = S > 16 ? 8 : 1;
     const int G = kDiag ? (env_override("B200CONV_REDG", Gd) == 8 ? 8 : 1) : Gd;
@@ -256,11 +263,41 @@ cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, in
     // a batch (plane < N) maps columns to (image, pixel): its own instantiation,
     // so the single-image store path is the plain one
     if (plane != N) {
-        if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, true>, W, S, slice, M, ldw, N, O, plane);
-        return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, true>, W, S, slice, M, ldw, N, O, plane);
+        if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, true>, W, S, slice, M, ldw, N, O, plane, po);
+        return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, true>, W, S, slice, M, ldw, N, O, plane, po);
     }
-    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, false>, W, S, slice, M, ldw, N, O, plane);
-    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, false>, W, S, slice, M, ldw, N, O, plane);
+    if (G == 8) return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<8, false>, W, S, slice, M, ldw, N, O, plane, po);
+    return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<1, false>, W, S, slice, M, ldw, N, O, plane, po);
+}
+
+__global__ void __launch_bounds__(256) peer_copy_kernel(const float *__restrict__ src, int64_t n, const PeerOut po) {
+    pdl_wait();
+    pdl_trigger();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = src[i];
+        if (po.mc) {
+            multimem_st_f32(po.mc + i, v);
+        } else {
+            for (int r = 0; r < po.n; ++r) po.p[r][i] = v;
+        }
+    }
+}
+
+cudaError_t launch_peer_copy(const float *src, int64_t n, cudaStream_t s) {
+    const PeerOut &po = peer_out();
+    if (n <= 0 || (!po.mc && po.n == 0)) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, peer_copy_kernel, src, n, po);
 }
 
 // empty kernel with the same launch attributes as the hot-path kernels: the

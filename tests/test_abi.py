@@ -22,7 +22,7 @@ def header_symbols():
 def test_library_exports_every_header_symbol():
     lib = conv.load()
     syms = header_symbols()
-    assert len(syms) == 20
+    assert len(syms) == 21
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(conv.EXPORTS)
@@ -222,3 +222,17 @@ def test_latency_model_b200_profile():
     assert m["threads_per_sm"] % 128 == 0 and m["v_s"] >= m["volume"]
     assert conv.load().conv_latency_model(7, (ctypes.c_double * 5)()) == 1        # unknown profile
     assert conv.load().conv_latency_model(0, None) == 2                           # null
+
+
+def test_allgather_argument_errors_before_device_access():
+    lib = conv.load()
+    f = 0x1000
+    peers = (ctypes.c_void_p * 2)(f, f)
+    A = lib.conv_multi_allgather_ex
+    assert A(f, 4, 8, 8, f, 3, 4, -1, 8, peers, 2, None, 0, None) == 1          # m0 < 0
+    assert A(f, 4, 8, 8, f, 3, 4, 6, 8, peers, 2, None, 0, None) == 1           # m0 + M > M_total
+    assert A(f, 4, 8, 8, f, 3, 4, 0, 8, peers, 0, None, 0, None) == 1           # no destination
+    assert A(f, 4, 8, 8, f, 3, 4, 0, 8, peers, 9, None, 0, None) == 1           # > 8 destinations
+    assert A(f, 4, 8, 8, f, 3, 4, 0, 8, None, 2, None, 0, None) == 2            # null peer array
+    assert A(f, 4, 8, 8, f, 3, 4, 0, 8, (ctypes.c_void_p * 2)(f, 0), 2, None, 0, None) == 2
+    assert A(f, 4, 8, 8, f, 3, 4, 0, 8, peers, 2, None, 5, None) == 4           # precision

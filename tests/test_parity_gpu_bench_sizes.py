@@ -228,3 +228,94 @@ def test_capture_on_a_fresh_stream_uses_graph_private_scratch(conv, prec, layer)
     torch.cuda.synchronize()
     for O in outs:
         assert torch.equal(O, ref)
+
+
+# ---------------------------------------------------------------- NEXT-2: epilogue-fused all-gather
+@pytest.mark.parametrize("prec,layer", [("fp32", 1), ("tf32", 2), ("bf16", 2), ("fp32", 7), ("tf32", 0),
+                                        ("bf16", 3), ("tf32", 7)])
+def test_allgather_fused_into_the_epilogue(conv, prec, layer):
+    """Four virtual ranks on one GPU, each owning M/4 filters, write their rows
+    straight into three 'peer' copies of O (conv_multi_allgather_ex): every
+    copy must equal the oracle's full O.  Layers cover the peer-aware stores
+    (KM-SIMT split-K reduce, KM-TC/G GEMM) and the copy fallback (implicit
+    KM-TC, KS-C3)."""
+    c = (list(synth.MULTI_LAYERS) + [synth.SHARD_SWEEP])[layer]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=600 + layer)
+    Ho, Wo = c["Wy"] - c["K"] + 1, c["Wx"] - c["K"] + 1
+    Id, Fd = torch.from_numpy(I).cuda().to(_dt(prec)), torch.from_numpy(F).cuda().to(_dt(prec))
+    peers = [torch.full((c["M"], Ho, Wo), float("nan"), device="cuda") for _ in range(3)]
+    world = 4
+    Ml = c["M"] // world
+    for r in range(world):
+        Fl = Fd[r * Ml:(r + 1) * Ml].contiguous()
+        conv.conv_multi_allgather_ex(Id, c["C"], c["Wx"], c["Wy"], Fl, c["K"], Ml, r * Ml, c["M"], peers,
+                                     None, prec)
+    torch.cuda.synchronize()
+    if c["M"] * Ho * Wo > 2_000_000:
+        idx = _sample_idx(c["M"] * Ho * Wo, 3000, layer)
+        Oo, A = oracle.conv_multi_sampled(I, F, idx)
+        for P in peers:
+            check(P.cpu().numpy().ravel()[idx], Oo, A, TAU[prec], f"allgather peer {prec} {c['name']}")
+    else:
+        Oo, A = oracle.conv_multi(I, F)
+        for P in peers:
+            check(P.cpu().numpy(), Oo, A, TAU[prec], f"allgather peer {prec} {c['name']}")
+    assert torch.equal(peers[0], peers[1]) and torch.equal(peers[0], peers[2])
+
+
+def _symm_worker(q, port):
+    """world-1 NCCL group: torch symmetric memory for O, the fused call through
+    its buffer pointers, and through its multicast address when the device
+    offers one (NVSwitch multicast: multimem.st in the epilogue)."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    out = {}
+    try:
+        from paper_2212_00404_b200 import conv
+        c = synth.MULTI_LAYERS[1]
+        I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=700)
+        Ho = c["Wy"] - c["K"] + 1
+        for prec in ("fp32", "tf32"):
+            O = symm.empty((c["M"], Ho, Ho), dtype=torch.float32, device="cuda")
+            O.fill_(float("nan"))
+            hdl = symm.rendezvous(O, dist.group.WORLD)
+            base = hdl.buffer_ptrs[0]
+            Id, Fd = torch.from_numpy(I).cuda(), torch.from_numpy(F).cuda()
+            conv.conv_multi_allgather_ex(Id, c["C"], c["Wx"], c["Wy"], Fd, c["K"], c["M"], 0, c["M"],
+                                         [base + (O.data_ptr() - base)], None, prec)
+            torch.cuda.synchronize()
+            out[prec] = O.cpu().numpy()
+            mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+            if mc:
+                O.fill_(float("nan"))
+                conv.conv_multi_allgather_ex(Id, c["C"], c["Wx"], c["Wy"], Fd, c["K"], c["M"], 0, c["M"],
+                                             [O.data_ptr()], mc + (O.data_ptr() - base), prec)
+                torch.cuda.synchronize()
+                out[prec + "_mc"] = O.cpu().numpy()
+        q.put(out)
+    except Exception as e:   # reported to the parent
+        q.put({"error": repr(e)[:300]})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allgather_through_torch_symmetric_memory():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_symm_worker, args=(q, _free_port()))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert "error" not in res, res
+    c = synth.MULTI_LAYERS[1]
+    I, F = synth.layer_inputs(c["C"], c["Wx"], c["Wy"], c["K"], c["M"], cfg_index=700)
+    Oo, A = oracle.conv_multi(I, F)
+    for k, O in res.items():
+        check(O, Oo, A, TAU[k.split("_")[0]], f"symmetric memory {k}")
+    print("symmetric-memory paths checked:", sorted(res))
