@@ -832,10 +832,10 @@ def run_ours(args):
 
     suite_res, calls, launch = (suite(args, conv, dev, stream, world, rank, pk, sms) if args.suite
                                 else (None, None, None))
-    if rank == 0 and world == 1 and calls is not None:
-        if args.layers:
+    if rank == 0 and world == 1:
+        if args.layers and calls is not None:
             detail["layers_b2b"] = layer_b2b(calls, launch, stream, pk, sms)
-        if args.cudnn:
+        if args.cudnn and calls is not None:
             detail["cudnn"] = cudnn_context(calls, stream, pk, sms)
         if args.batched:
             detail["batched"] = batched(args, conv, dev, stream, pk)

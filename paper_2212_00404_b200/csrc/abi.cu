@@ -481,6 +481,27 @@ int conv_multi_pad_ex(const void *I, int N, int C, int Wx, int Wy, const void *F
     if ((st = check_ptrs(I, F, O, e))) return st;
     if ((st = check_device())) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (precision != CONV_FP32) {
+        // the implicit tensor-core kernel (every TF32 / BF16 batch; single
+        // images unless KM-TC/G takes them) reads the padded copy with its row
+        // stride rounded up to 16 B: the patch keeps one 2-D TMA box per stage
+        // and the offset-table gather (30-wide BF16 rows are 60 B, not a 16-B
+        // multiple); the columns past Wx + 2 pad are zeros whose outputs the
+        // kernel drops (valid width Wxp)
+        const bool bf16 = precision == CONV_BF16;
+        const int v = 16 / e, Wps = (Wxp + v - 1) / v * v;
+        conv_plan tmp;
+        if (Wps != Wxp && !c3_layer(C, Wxp, Wyp, K, M) && (int64_t)N * C * Wps * Wyp <= INT_MAX &&
+            (N > 1 || plan_multi_gemm(C, Wxp, Wyp, K, M, bf16, &tmp) != 0)) {
+            void *Ip = padbuf_get((size_t)N * C * Wps * Wyp * e, s);
+            if (!Ip) return CONV_E_LAUNCH;
+            if ((st = launch_status(launch_pad(I, N * C, Wx, Wy, pad, e, Ip, s, Wps)))) return st;
+            set_valid_width(Wxp);
+            const cudaError_t er = launch_multi_tc(Ip, C, Wps, Wyp, F, K, M, O, bf16, s, N);
+            set_valid_width(0);
+            return launch_status(er);
+        }
+    }
     void *Ip = padbuf_get((size_t)N * C * Wxp * Wyp * e, s);
     if (!Ip) return CONV_E_LAUNCH;
     if ((st = launch_status(launch_pad(I, N * C, Wx, Wy, pad, e, Ip, s)))) return st;

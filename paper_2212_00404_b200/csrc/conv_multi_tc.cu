@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
             const void *__restrict__ Iv, const void *__restrict__ Fv, int C, int Wx, int Wy,
             int K, int M, float *__restrict__ O, int kb_per_split, int patch2d, int dbg_in,
-            float *__restrict__ Wk, int Nimg) {
+            float *__restrict__ Wk, int Nimg, int Wv) {
     const int dbg = kDiag ? dbg_in : 0;
     using Tr = TcTraits<kTF32>;
     using T = typename Tr::T;
@@ -150,7 +150,9 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
     const int Ktot = C * KK;
     const int HW = Wx * Wy;
     const int64_t CHW = (int64_t)C * HW;
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    // Wv: valid input width (padded calls: the row stride Wx is rounded up to
+    // 16 B; columns >= Wv are zeros whose outputs are wide-pixel garbage)
+    const int Ho = Wy - K + 1, Wo = (Wv > 0 ? Wv : Wx) - K + 1;
     // batch: blockIdx.y = image * (pixel tiles per image) + pixel tile
     const int npt_img = gridDim.y / Nimg;
     const int img = blockIdx.y / npt_img;
@@ -578,14 +580,14 @@ constexpr int kTpThreads = 32 * (kTpEpiWarp + 4);
 template <bool kTF32, int BN>
 __global__ void __launch_bounds__(kTpThreads, 1)
 kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
-                    int C, int Wx, int Wy, int K, int M, float *__restrict__ O, int Nimg, int tiles_y) {
+                    int C, int Wx, int Wy, int K, int M, float *__restrict__ O, int Nimg, int tiles_y, int Wv) {
     using Tr = TcTraits<kTF32>;
     constexpr int BK = Tr::kBK;
     constexpr int B_BYTES = BN * 128;
     constexpr uint32_t IDESC = umma_idesc(Tr::kFmt, kTcBM, BN);
     const int KK = K * K;
     const int Ktot = C * KK;
-    const int Ho = Wy - K + 1, Wo = Wx - K + 1;
+    const int Ho = Wy - K + 1, Wo = (Wv > 0 ? Wv : Wx) - K + 1;   // Wv: see kmtc_kernel
     const int nkb = Ktot / BK;                           // plan: Ktot % BK == 0
     const TcGeom geo = tc_geom(Wx, K, BN, Tr::kElem, true);
     const int NS = geo.stages;
@@ -885,7 +887,8 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
         const size_t bytes = (size_t)p.cluster_x * p.grid_y * p.grid_z * BN * kTcBM * 4;
         Wk = static_cast<float *>(workspace_get(bytes, s));
     }
-    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg, Wk, N);
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, I, F, C, Wx, Wy, K, M, O, kb_per_split, patch2d, dbg, Wk, N,
+                              valid_width());
 }
 
 template <bool kTF32, int BN>
@@ -906,7 +909,7 @@ static cudaError_t launch_tc_persist(const conv_plan &p, const CUtensorMap &tf, 
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tf, ti, C, Wx, Wy, K, M, O, N, tiles_y);
+    return cudaLaunchKernelEx(&cfg, kern, tf, ti, C, Wx, Wy, K, M, O, N, tiles_y, valid_width());
 }
 
 template <bool kTF32, int BN>

@@ -115,6 +115,13 @@ __device__ __forceinline__ void out_store(const PeerOut &po, float *O, int64_t i
 // final stores are not peer-aware)
 cudaError_t launch_peer_copy(const float *src, int64_t n, cudaStream_t s);
 
+// Valid input width of the map the KM-TC kernels read (padded calls, NEXT-3):
+// the zero-padded copy of I has 16-B-multiple row strides (Wx) so the patch
+// keeps its 2-D TMA boxes, and only Wv - K + 1 output columns are real.
+// 0 = Wx.  Thread-local, set by conv_multi_pad_ex around its launch.
+void set_valid_width(int Wv);
+int valid_width();
+
 // Every ABI entry point holds a CallScope for the duration of the call: the
 // graph-private scratch allocated while a stream is being captured is freed
 // (cudaFreeAsync, in stream order) when the outermost scope ends.
@@ -136,7 +143,8 @@ void *auxbuf_get(size_t bytes, cudaStream_t s);
 // Fp[m][k] = F[m][k] (k < Ktot), 0 (Ktot <= k < Kp)
 cudaError_t launch_pad_rows(const void *F, int M, int Ktot, int Kp, int elem, void *Fp, cudaStream_t s);
 // Ip = I with a zero border of `pad` on every side of each of NC planes
-cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s);
+cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s,
+                       int Wps = 0);   // Wps: row stride of Ip (>= Wx + 2 pad; 0 = Wx + 2 pad), extra columns zero
 // O[m][n] = sum_{s<S} W[s*slice + m*ldw + n] in order s = 0..S-1; plane < N:
 // a batch, column n is pixel n % plane of image n / plane, O [N/plane][M][plane]
 cudaError_t launch_splitk_reduce(const float *W, int S, int64_t slice, int M, int ldw, int N, float *O,

@@ -47,7 +47,10 @@ thread_local int t_call_depth = 0;
 namespace {
 thread_local PeerOut t_peer_out = {};
 }
+thread_local int t_valid_width = 0;
 const PeerOut &peer_out() { return t_peer_out; }
+void set_valid_width(int Wv) { t_valid_width = Wv; }
+int valid_width() { return t_valid_width; }
 void set_peer_out(const PeerOut *po) { t_peer_out = po ? *po : PeerOut{}; }
 
 CallScope::CallScope() { ++t_call_depth; }
@@ -167,14 +170,15 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
     }
 }
 
-// Ip[n][c][y][x] = I[n][c][y - pad][x - pad] inside, 0 in the border
-// (elem = 4 or 2 bytes; one element per thread, grid-stride).
+// Ip[n][c][y][x] = I[n][c][y - pad][x - pad] inside, 0 in the border and in
+// the columns Wx + 2 pad <= x < Wp of a wider row stride Wp (elem = 4 or 2
+// bytes; one element per thread, grid-stride).
 template <typename T>
 __global__ void __launch_bounds__(256)
-pad_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restrict__ Ip) {
+pad_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restrict__ Ip, int Wp) {
     pdl_wait();
     pdl_trigger();
-    const int Wp = Wx + 2 * pad, Hp = Wy + 2 * pad;
+    const int Hp = Wy + 2 * pad;
     const int64_t total = (int64_t)NC * Hp * Wp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t plane = i / ((int64_t)Hp * Wp);
@@ -186,8 +190,57 @@ pad_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restri
     }
 }
 
-cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s) {
-    const int64_t total = (int64_t)NC * (Wy + 2 * pad) * (Wx + 2 * pad);
+// The same with 16-B output rows (Wp * sizeof(T) a multiple of 16, Ip 16-B
+// aligned): one 16-B vector of a padded row per thread, one index decode per
+// vector instead of per element.
+template <typename T>
+__global__ void __launch_bounds__(256)
+pad_vec_kernel(const T *__restrict__ I, int NC, int Wx, int Wy, int pad, T *__restrict__ Ip, int Wp) {
+    constexpr int V = 16 / sizeof(T);
+    pdl_wait();
+    pdl_trigger();
+    const int Hp = Wy + 2 * pad, nv = Wp / V;
+    const int64_t total = (int64_t)NC * Hp * nv;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / nv;                      // plane * Hp + yp
+        const int xv = (int)(i - row * nv) * V;
+        const int64_t plane = row / Hp;
+        const int y = (int)(row - plane * Hp) - pad;
+        union { uint4 u; T e[V]; } v;
+        const T *src = I + (plane * Wy + y) * Wx;
+        const bool yok = y >= 0 && y < Wy;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const int x = xv + e - pad;
+            v.e[e] = (yok && x >= 0 && x < Wx) ? src[x] : T(0.f);
+        }
+        reinterpret_cast<uint4 *>(Ip)[i] = v.u;
+    }
+}
+
+cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem, void *Ip, cudaStream_t s,
+                       int Wps) {
+    if (Wps < Wx + 2 * pad) Wps = Wx + 2 * pad;
+    if ((Wps * elem) % 16 == 0 && reinterpret_cast<uintptr_t>(Ip) % 16 == 0) {
+        const int64_t vecs = (int64_t)NC * (Wy + 2 * pad) * (Wps * elem / 16);
+        int64_t blocks = (vecs + 255) / 256;
+        if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (elem == 2)
+            return cudaLaunchKernelEx(&cfg, pad_vec_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16 *>(I),
+                                      NC, Wx, Wy, pad, static_cast<__nv_bfloat16 *>(Ip), Wps);
+        return cudaLaunchKernelEx(&cfg, pad_vec_kernel<float>, static_cast<const float *>(I), NC, Wx, Wy, pad,
+                                  static_cast<float *>(Ip), Wps);
+    }
+    const int64_t total = (int64_t)NC * (Wy + 2 * pad) * Wps;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
     cudaLaunchConfig_t cfg = {};
@@ -201,9 +254,9 @@ cudaError_t launch_pad(const void *I, int NC, int Wx, int Wy, int pad, int elem,
     cfg.numAttrs = 1;
     if (elem == 2)
         return cudaLaunchKernelEx(&cfg, pad_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16 *>(I), NC, Wx,
-                                  Wy, pad, static_cast<__nv_bfloat16 *>(Ip));
+                                  Wy, pad, static_cast<__nv_bfloat16 *>(Ip), Wps);
     return cudaLaunchKernelEx(&cfg, pad_kernel<float>, static_cast<const float *>(I), NC, Wx, Wy, pad,
-                              static_cast<float *>(Ip));
+                              static_cast<float *>(Ip), Wps);
 }
 
 // Fp[m][k] = F[m][k] for k < Ktot, 0 for Ktot <= k < Kp (elem-byte elements)
