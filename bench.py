@@ -18,8 +18,10 @@ N > 1 rank 0 also times the full-M layer alone (`t1_us`) in the same run.
 
 Timing: W warm-up steps, then EXACTLY K steps between a barrier + synchronize
 on both sides; device time from CUDA events on the launching stream; max over
-ranks.  Each precision call is one CUDA graph (its 2 PDL-chained kernels);
-events between them attribute the step to the kernels live.  Two buffer sets
+ranks.  A step is one CUDA graph (the three precision calls, 6 kernels,
+PDL-chained).  Each kernel's share of the step is what the step loses without
+it (full-step graph vs step-minus-precision graphs, replayed interleaved right
+after the timed region), scaled to the timed region.  Two buffer sets
 (F, O) alternate between steps: 2 x (75.5 + 75.5 + 37.7) MB of filters pass
 through between re-reads of a set, > 3x the 126 MB L2 ("inputs larger than
 L2").  NVML samples SM clocks and throttle reasons every ~1 ms during the
@@ -273,41 +275,59 @@ def headline(args, conv, dev, stream, world, rank, pk, sms):
             for p in args.precs:
                 call(p, j)
     stream.synchronize()
+    # the step = one CUDA graph per buffer set: the precision calls PDL-chained
+    # (each call's prologue overlaps the previous one's tail; no graph or
+    # event boundary inside the step)
+    step_g = [_capture(stream, lambda j=j: [call(p, j) for p in args.precs]) for j in range(NSET)]
     graphs = {(p, j): _capture(stream, lambda p=p, j=j: call(p, j)) for p in args.precs for j in range(NSET)}
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
-            for p in args.precs:
-                graphs[(p, s % NSET)].replay()
+            step_g[s % NSET].replay()
     stream.synchronize()
 
     # ---- timed region: exactly K steps
     P = len(args.precs)
-    evs = [[_ev() for _ in range(P + 1)] for _ in range(args.steps)]
-    with torch.cuda.stream(stream):               # create the events outside the timed region
-        for e in evs:
-            for x in e:
-                x.record(stream)
-    stream.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    t0, t1 = _ev(), _ev()
     with ClockSampler(dev.index) as clk, torch.cuda.stream(stream):
         clk.mark_start()
+        t0.record(stream)
         for s in range(args.steps):
-            e = evs[s]
-            e[0].record(stream)
-            for i, p in enumerate(args.precs):
-                graphs[(p, s % NSET)].replay()
-                e[i + 1].record(stream)
+            step_g[s % NSET].replay()
+        t1.record(stream)
         stream.synchronize()
         clk.mark_end()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    total_ms = evs[0][0].elapsed_time(evs[-1][P])
-    per_p_ms = [sum(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)) for i in range(P)]
-    total_ms, *per_p_ms = _max_over_ranks([total_ms] + per_p_ms, dev, world)
+    total_ms = _max_over_ranks([t0.elapsed_time(t1)], dev, world)[0]
     ms_step = total_ms / args.steps
+    # ---- each kernel's live share of the PDL-chained step (outside the timed
+    # region): what the step loses without it — R replays of the full step and
+    # of each step-minus-precision graph, interleaved over 4 rounds
+    minus = [_capture(stream, lambda i=i: [call(q, 0) for q in args.precs if q != args.precs[i]]) for i in range(P)]
+    R = 50
+
+    def _rep_ms(g):
+        a, b = _ev(), _ev()
+        a.record(stream)
+        for _ in range(R):
+            g.replay()
+        b.record(stream)
+        stream.synchronize()
+        return a.elapsed_time(b) / R
+    full_s, minus_s = [], [[] for _ in range(P)]
+    with torch.cuda.stream(stream):
+        for _ in range(4):
+            full_s.append(_rep_ms(step_g[0]))
+            for i in range(P):
+                minus_s[i].append(_rep_ms(minus[i]))
+    full = statistics.median(full_s)
+    per_p_ms = [max(full - statistics.median(minus_s[i]), 1e-4) * args.steps for i in range(P)]
+    scale = total_ms / max(sum(per_p_ms), 1e-9)               # shares of the timed region
+    per_p_ms = _max_over_ranks([x * scale for x in per_p_ms], dev, world)
     flop_p = c["flop"]                                    # whole layer (all ranks)
     value = P * flop_p / (ms_step * 1e-3) / 1e9
 
