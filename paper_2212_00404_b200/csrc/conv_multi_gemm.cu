@@ -417,7 +417,14 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N
     // with >= 4 filter tiles (ResNet 7x7: 8.4 vs 11.8 us bf16; configs[4]
     // sweep: 24.4 vs 30.2 us bf16).  Pixels-on-M layers stay on the implicit
     // kernel (e.g. 28x28x256: 10.1 vs 16.9 us), B200CONV_GM=2 forces this path.
-    if (!(p.modeF && p.tilesA >= 4) && env_override("B200CONV_GM", 1) != 2 && sd == 1) return p;
+    // TF32 (round 2, tools/gm_vs_implicit.py): the GEMM re-streams a 4-byte X
+    // tile per filter tile; where the implicit kernel's wide-pixel waste is
+    // small ((K-1)/Wx <= 1/6: the 14x14 layers, 17 %) it builds A on chip for
+    // less — configs[4] at M = 4096 / 2048 / 1024 / 512: 27.8 / 19.8 / 15.7 /
+    // 12.3 us against 32.5 / 23.0 / 18.2 / 15.5 us.  BF16 keeps the GEMM
+    // (24.4 vs 29.0 us at M = 4096), as do the 7x7 layers (40 % waste).
+    const bool tf32_implicit = !bf16 && 6 * (K - 1) <= Wx;
+    if ((!(p.modeF && p.tilesA >= 4) || tf32_implicit) && env_override("B200CONV_GM", 1) != 2 && sd == 1) return p;
     const int tiles = p.tilesA * p.tilesB;
     // split the k loop over a cluster: fill the SMs, >= 2 k-blocks per split,
     // and only when the saved k-loop time beats the ~3 us partial exchange

@@ -232,7 +232,7 @@ def test_capture_on_a_fresh_stream_uses_graph_private_scratch(conv, prec, layer)
 
 # ---------------------------------------------------------------- NEXT-2: epilogue-fused all-gather
 @pytest.mark.parametrize("prec,layer", [("fp32", 1), ("tf32", 2), ("bf16", 2), ("fp32", 7), ("tf32", 0),
-                                        ("bf16", 3), ("tf32", 7)])
+                                        ("bf16", 3), ("tf32", 7), ("bf16", 7)])
 def test_allgather_fused_into_the_epilogue(conv, prec, layer):
     """Four virtual ranks on one GPU, each owning M/4 filters, write their rows
     straight into three 'peer' copies of O (conv_multi_allgather_ex): every
