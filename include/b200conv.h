@@ -58,7 +58,8 @@
  *   B200CONV_TC_BN=32..256  KM-TC filter-tile width
  *   B200CONV_TC_SPLIT=S     KM-TC k split S
  *   B200CONV_TC_PERSIST=0   no persistent KM-TC for batched calls
- *   B200CONV_TC_DSMEM=1     KM-TC split-K partials reduced through DSMEM
+ *   B200CONV_TC_DSMEM=0|1   KM-TC split-K partials exchanged through L2 (0) or
+ *                           DSMEM (1); default DSMEM for splits <= 4
  *   B200CONV_SIMT_FORCE=t,S,ws  KM-SIMT thread tile t, channel split S, ws=1:
  *                           reduced through the workspace
  *   B200CONV_C3=0           no KS-C3 (C = 3 stems take the general kernels)

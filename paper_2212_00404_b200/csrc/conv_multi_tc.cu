@@ -883,7 +883,12 @@ static cudaError_t launch_tc(const conv_plan &p, const CUtensorMap &tf, const CU
     // split-K partials go through the L2 workspace (DSMEM reduction when the
     // workspace cannot grow during stream capture, or with B200CONV_TC_DSMEM=1)
     float *Wk = nullptr;
-    if (p.cluster_x > 1 && env_override("B200CONV_TC_DSMEM", 0) != 1) {
+    // split-K exchange: the L2 round trip (bulk store + bulk loads, 2 x the
+    // tile per CTA at ~50 B/clk) or DSMEM ((S-1)/S of the tile at ~20 B/clk):
+    // DSMEM wins for S <= 4 (configs[4] TF32: 25.9 vs 27.9 us), L2 above
+    // (ResNet / AlexNet / target layers, S = 5..15: 0.5-1 us faster)
+    const int dsmem_default = p.cluster_x <= 4 ? 1 : 0;
+    if (p.cluster_x > 1 && env_override("B200CONV_TC_DSMEM", dsmem_default) != 1) {
         const size_t bytes = (size_t)p.cluster_x * p.grid_y * p.grid_z * BN * kTcBM * 4;
         Wk = static_cast<float *>(workspace_get(bytes, s));
     }
