@@ -659,6 +659,7 @@ extern "C" B200CONV_API int conv_diag_ks_stamps(unsigned long long *host) { retu
 extern "C" B200CONV_API int conv_diag_ks_fine(unsigned long long *host) { return ks_read_fine(host); }
 extern "C" B200CONV_API int conv_diag_simt_stamps(unsigned long long *host) { return simt_read_stamps(host); }
 extern "C" B200CONV_API int conv_diag_tc_cta_stamps(unsigned long long *host) { return tc_read_cta_stamps(host); }
+extern "C" B200CONV_API int conv_diag_gm_cta_stamps(unsigned long long *host) { return gm_read_cta_stamps(host); }
 extern "C" B200CONV_API int conv_diag_max_clusters(int kernel, int cluster, int smem_bytes) {
     return kernel == 2 ? tc_max_clusters(cluster, smem_bytes) : simt_max_clusters(cluster, smem_bytes);
 }

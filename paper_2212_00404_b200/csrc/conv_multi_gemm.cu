@@ -94,7 +94,21 @@ struct GmArgs {
     float *O;
     float *Wk;        // split-K partials [S][tiles][BN][128] (nullptr: DSMEM reduction)
     PeerOut po;       // NEXT-2: extra / multicast destinations of every O store
+    int dbg;          // diagnostics (kDiag builds only)
 };
+
+// diagnostics (-DB200CONV_DIAG builds, B200CONV_GM_DBG=1): per-CTA globaltimer
+// stamps [start, after griddepcontrol.wait, first stage full (MMA warp),
+// MMAs done (epilogue), epilogue done, cluster barrier passed, end << 8 | smid]
+__device__ unsigned long long g_gm_cta[8 * 1024];
+int gm_read_cta_stamps(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, g_gm_cta, sizeof(g_gm_cta)) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ unsigned long long gm_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <bool kTF32, int BN, bool kModeF>
 __global__ void __launch_bounds__(kGmThreads, 1)
@@ -126,6 +140,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int kb1 = min(g.nkb, kb0 + g.kbps);
     const int niter = kb1 > kb0 ? kb1 - kb0 : 0;
     const uint32_t warp = warp_id(), lane = lane_id();
+    const unsigned cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool tl = kDiag && g.dbg && cta_lin < 1024;
+    if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin] = gm_gtimer();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -142,6 +159,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t tmem = *tmem_slot;
     pdl_wait();                                       // kernel 1 (im2col) complete and visible
     pdl_trigger();
+    if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 1] = gm_gtimer();
 
     if (warp == 0) {
         // -------------------------------------------- TMA producer
@@ -164,6 +182,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const int s = i % NS;
                 mbar_wait(&full[s], (i / NS) & 1);
                 tc_fence_after();
+                if (tl && i == 0) g_gm_cta[8 * cta_lin + 2] = gm_gtimer();
                 const uint32_t a_addr = smem_u32(smem + s * STAGE);
                 const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
@@ -184,6 +203,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_wait(tmem_full, 0);
             tc_fence_after();
         }
+        if (tl && warp == 2 && lane == 0) g_gm_cta[8 * cta_lin + 3] = gm_gtimer();
         constexpr int NCB = (BN + 31) / 32;           // 32-column blocks; BN % 32 == 16: a 16-column tail
 #pragma unroll 1
         for (int cb = 0; cb < NCB; ++cb) {
@@ -249,6 +269,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         tc_fence_before();
     }
     __syncthreads();
+    if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 4] = gm_gtimer();
 
     if (S > 1) {
         // ---------------------------------------------- split-K reduction
@@ -260,6 +281,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             fence_proxy_async_global();
         }
         cluster_sync_all();
+        if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 5] = gm_gtimer();
         const int nlo = split * BN / S;               // columns [nlo, nhi) reduced by this rank
         const int rows = (split + 1) * BN / S - nlo;
         float *slices = P;                            // [S][rows][128]
@@ -322,6 +344,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TCOLS>(tmem);
+    }
+    if (tl && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_gm_cta[8 * cta_lin + 6] = gm_gtimer() << 8 | smid;
     }
 }
 
@@ -561,6 +588,7 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     }
     GmArgs g;
     g.po = N == 1 ? peer_out() : PeerOut{};
+    g.dbg = kDiag ? env_override("B200CONV_GM_DBG", 0) : 0;
     g.nkb = p.nkb;
     g.kbps = p.kbps;
     g.M = M;

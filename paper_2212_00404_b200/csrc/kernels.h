@@ -164,6 +164,7 @@ int tc_read_stamps(unsigned long long *host);
 int ks_read_stamps(unsigned long long *host);
 int ks_read_fine(unsigned long long *host);
 int tc_read_cta_stamps(unsigned long long *host);
+int gm_read_cta_stamps(unsigned long long *host);
 int simt_max_clusters(int cluster, int smem);
 int simt_read_stamps(unsigned long long *host);
 
