@@ -55,6 +55,8 @@
  *   B200CONV_PDL=0          no programmatic dependent launch
  *   B200CONV_GM=0|2         KM-TC/G im2col+GEMM path off | forced where legal
  *   B200CONV_GM_SPLIT=S     KM-TC/G k split (cluster size) S
+ *   B200CONV_GM_DSMEM=1     KM-TC/G split-K partials through DSMEM instead of
+ *                           the L2 workspace
  *   B200CONV_TC_BN=32..256  KM-TC filter-tile width
  *   B200CONV_TC_SPLIT=S     KM-TC k split S
  *   B200CONV_TC_PERSIST=0   no persistent KM-TC for batched calls

@@ -47,24 +47,17 @@ constexpr int kGmSmemMax = 225 * 1024;
 // ---------------------------------------------------------------- kernel 1
 // X[p][k] for p < P, k < Kp (row stride Kp; zero for k >= C*K*K and outside
 // the channel).  One 16-B vector of consecutive k per thread: coalesced rows.
-// Pixel p = y*Wp + x reads input row y*sd, column x*sd: stride 1 uses wide
-// pixels (Wp = Wx, so the input offset is p itself), stride sd > 1 compact
-// ones (Wp = Wo).
+// Pixel p = y*Wp + x (compact, Wp = Wo) reads input row y*sd, column x*sd.
 // Batched (strided calls): pixels p < Ptot = N*Pimg, image n = p / Pimg reads
 // I[n]; rows Ptot <= p < P are zero.
 template <typename T>
-__global__ void __launch_bounds__(256)
-im2col_kernel(const T *__restrict__ I, int C, int Wx, int Wy, int K, int P, int Kp, T *__restrict__ X,
-              int sd, int Wp, int Pimg, int Ptot) {
-    constexpr int V = 16 / sizeof(T);
-    const int KK = K * K, HW = Wx * Wy, Ktot = C * KK;
-    const int nv = Kp / V;
-    const int64_t total = (int64_t)P * nv;
-    pdl_wait();
-    pdl_trigger();
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int pg = (int)(idx / nv), kv = (int)(idx - (int64_t)pg * nv);
+struct Im2col {
+    const T *I;
+    int C, Wx, Wy, K, Kp, sd, Wp, Pimg, Ptot;
+    // the 16-B vector kv (V = 16 / sizeof(T) consecutive k) of X row pg
+    __device__ __forceinline__ uint4 vec(int pg, int kv) const {
+        constexpr int V = 16 / sizeof(T);
+        const int KK = K * K, HW = Wx * Wy, Ktot = C * KK;
         const int n = pg / Pimg, p = pg - n * Pimg;          // image, pixel within the image
         const T *In = I + (int64_t)n * C * HW;
         const int py = p / Wp;
@@ -80,7 +73,22 @@ im2col_kernel(const T *__restrict__ I, int C, int Wx, int Wy, int K, int P, int 
             ++k;
             if (++c == K) { c = 0; if (++r == K) { r = 0; ++ch; } }
         }
-        *reinterpret_cast<uint4 *>(X + (int64_t)pg * Kp + (int64_t)kv * V) = v.u;
+        return v.u;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+im2col_kernel(const Im2col<T> a, int P, T *__restrict__ X) {
+    constexpr int V = 16 / sizeof(T);
+    const int nv = a.Kp / V;
+    const int64_t total = (int64_t)P * nv;
+    pdl_wait();
+    pdl_trigger();
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int pg = (int)(idx / nv), kv = (int)(idx - (int64_t)pg * nv);
+        *reinterpret_cast<uint4 *>(X + (int64_t)pg * a.Kp + (int64_t)kv * V) = a.vec(pg, kv);
     }
 }
 
@@ -92,10 +100,15 @@ struct GmArgs {
     int N;            // images (strided batched calls: compact pixels p = (n*Ho + y)*Wo + x)
     int stages, stage_bytes;
     float *O;
-    float *Wk;        // split-K partials [S][tiles][BN][128] (nullptr: DSMEM reduction)
+    float *Wk;        // split-K partials [S][tiles][BN][PS] (nullptr: DSMEM reduction)
     PeerOut po;       // NEXT-2: extra / multicast destinations of every O store
     int dbg;          // diagnostics (kDiag builds only)
 };
+
+// Filters-on-M partial / transpose tile in shared memory: [BN pixels][kGmPS]
+// floats, filter rows contiguous (the 4-float pad keeps both the row-per-lane
+// writes from TMEM and the pixel-per-lane float4 reads conflict-free).
+constexpr int kGmPS = kGmBM + 4;
 
 // diagnostics (-DB200CONV_DIAG builds, B200CONV_GM_DBG=1): per-CTA globaltimer
 // stamps [start, after griddepcontrol.wait, first stage full (MMA warp),
@@ -130,7 +143,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t *tmem_full = empty + kGmMaxStages;
     uint64_t *red_bar = tmem_full + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(red_bar + 1);
-    float *P = reinterpret_cast<float *>(smem);       // [BN][128] partial tile, aliases the stages
+    float *P = reinterpret_cast<float *>(smem);       // partial / transpose tile, aliases the stages
 
     const int S = gridDim.x, split = blockIdx.x;
     const int a0 = blockIdx.y * kGmBM;                // first A row of the tile
@@ -221,42 +234,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                 for (int j = 0; j < 32; ++j) r[j] = 0u;
             }
-            if (S == 1) {
-                if constexpr (kModeF) {
-                    // row = filter, columns = pixels b0 + cb*32 + j
-                    const int m = a0 + row;
-                    if (m < g.M && g.N > 1) {
-                        for (int j = 0; j < ncol; ++j) {
-                            const int p = b0 + cb * 32 + j;
-                            int y = p / g.Wx;
-                            const int x = p - y * g.Wx, n = y / g.Ho;
-                            y -= n * g.Ho;
-                            if (n < g.N && x < g.Wo)
-                                out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, __uint_as_float(r[j]));
-                        }
-                    } else if (m < g.M) {
-                        const int p = b0 + cb * 32;
-                        int y = p / g.Wx, x = p - y * g.Wx;
-                        const int64_t orow = (int64_t)m * plane;
+            if constexpr (kModeF) {
+                // row = filter, column = pixel: P[pixel][filter] (stored below,
+                // pixel-fastest, so every warp store is one run of pixels)
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if (y < g.Ho && x < g.Wo) out_store(g.po, g.O, orow + y * g.Wo + x, __uint_as_float(r[j]));
-                            if (++x == g.Wx) { x = 0; ++y; }
-                        }
-                    }
-                } else {
-                    // row = pixel, columns = filters b0 + cb*32 + j
-                    const int p = a0 + row;
-                    int y = p / g.Wx;
-                    const int x = p - y * g.Wx, n = y / g.Ho;      // n = image (0 unless batched)
-                    y -= n * g.Ho;
-                    if (n < g.N && x < g.Wo) {
-                        const int64_t o = (int64_t)n * g.M * plane + (int64_t)y * g.Wo + x;
+                for (int j = 0; j < 32; ++j)
+                    if (j < ncol) P[(cb * 32 + j) * kGmPS + row] = __uint_as_float(r[j]);
+            } else if (S == 1) {
+                // row = pixel, columns = filters b0 + cb*32 + j
+                const int p = a0 + row;
+                int y = p / g.Wx;
+                const int x = p - y * g.Wx, n = y / g.Ho;      // n = image (0 unless batched)
+                y -= n * g.Ho;
+                if (n < g.N && x < g.Wo) {
+                    const int64_t o = (int64_t)n * g.M * plane + (int64_t)y * g.Wo + x;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int m = b0 + cb * 32 + j;
-                            if (m < g.M) out_store(g.po, g.O, o + (int64_t)m * plane, __uint_as_float(r[j]));
-                        }
+                    for (int j = 0; j < 32; ++j) {
+                        const int m = b0 + cb * 32 + j;
+                        if (m < g.M) out_store(g.po, g.O, o + (int64_t)m * plane, __uint_as_float(r[j]));
                     }
                 }
             } else {
@@ -271,8 +266,68 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     __syncthreads();
     if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 4] = gm_gtimer();
 
-    if (S > 1) {
-        // ---------------------------------------------- split-K reduction
+    if constexpr (kModeF) {
+        // ---------------------------------------------- store / split-K reduction
+        // rank `split` owns pixels [nlo, nhi) of the tile (all S ranks' partials
+        // summed in rank order: deterministic); threads run along pixels, so
+        // each of the four filter rows a thread stores is a coalesced warp store
+        const int plane = g.Ho * g.Wo;
+        const int nlo = split * BN / S, nhi = (split + 1) * BN / S, np = nhi - nlo;
+        const float *src = P;                         // [.][kGmPS] rows of pixel nlo.. (local / workspace)
+        int src_p0 = 0;
+        if (S > 1 && g.Wk) {
+            if (threadIdx.x == 0) {
+                bulk_store(g.Wk + ((int64_t)split * gridDim.y * gridDim.z + tile_lin) * BN * kGmPS, P,
+                           (uint32_t)(BN * kGmPS * 4));
+                bulk_commit();
+                bulk_wait<0>();
+                fence_proxy_async_global();
+            }
+            cluster_sync_all();
+            if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 5] = gm_gtimer();
+            if (threadIdx.x == 0) {
+                const int64_t wslice = (int64_t)gridDim.y * gridDim.z * BN * kGmPS;
+                const float *wt = g.Wk + ((int64_t)tile_lin * BN + nlo) * kGmPS;
+                const uint32_t bytes = (uint32_t)(np * kGmPS * 4);
+                mbar_arrive_expect_tx(red_bar, bytes * S);
+                for (int t = 0; t < S; ++t) bulk_load(P + t * np * kGmPS, wt + t * wslice, bytes, red_bar);
+            }
+            mbar_wait(red_bar, 0);
+            src_p0 = nlo;
+        } else if (S > 1) {
+            cluster_sync_all();                       // every rank's partial is in its smem
+            if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 5] = gm_gtimer();
+        }
+        const uint32_t Pbase = smem_u32(P);
+        for (int idx = threadIdx.x; idx < np * (kGmBM / 4); idx += kGmThreads) {
+            const int qd = idx / np, p = nlo + (idx - qd * np);
+            const int m0 = a0 + 4 * qd;
+            float4 v;
+            if (S > 1 && g.Wk) {
+                const float *sl = src + (p - src_p0) * kGmPS + 4 * qd;
+                v = *reinterpret_cast<const float4 *>(sl);
+                for (int t = 1; t < S; ++t) {
+                    const float4 u = *reinterpret_cast<const float4 *>(sl + t * np * kGmPS);
+                    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+                }
+            } else if (S > 1) {
+                v = dsmem_sum_ranks<kGmMaxSplit>(Pbase + (uint32_t)((p * kGmPS + 4 * qd) * 4), S);
+            } else {
+                v = *reinterpret_cast<const float4 *>(P + p * kGmPS + 4 * qd);
+            }
+            const int pg = b0 + p;                    // compact pixel over all images
+            const int n = pg / plane;
+            if (n < g.N) {
+                const int64_t o = ((int64_t)n * g.M + m0) * plane + (pg - n * plane);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (m0 + e < g.M) out_store(g.po, g.O, o + (int64_t)e * plane, vv[e]);
+            }
+        }
+        if (S > 1 && !g.Wk) cluster_sync_all();      // keep this CTA's partial alive for the others
+    } else if (S > 1) {
+        // ---------------------------------------------- split-K reduction (pixels on M)
         if (g.Wk && threadIdx.x == 0) {
             bulk_store(g.Wk + ((int64_t)split * gridDim.y * gridDim.z + tile_lin) * BN * kGmBM, P,
                        (uint32_t)(BN * kGmBM * 4));
@@ -311,31 +366,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 v = dsmem_sum_ranks<kGmMaxSplit>(Pbase + (uint32_t)((nl * kGmBM + row0) * 4), S);
             }
             const float vv[4] = {v.x, v.y, v.z, v.w};
-            if constexpr (kModeF) {
-                // column = pixel, rows = 4 filters
-                const int p = b0 + nl;
-                int y = p / g.Wx;
-                const int x = p - y * g.Wx, n = y / g.Ho;
-                y -= n * g.Ho;
-                if (n < g.N && x < g.Wo) {
+            // column = filter, rows = 4 pixels
+            const int m = b0 + nl;
+            if (m < g.M) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int m = a0 + row0 + e;
-                        if (m < g.M) out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, vv[e]);
-                    }
-                }
-            } else {
-                // column = filter, rows = 4 pixels
-                const int m = b0 + nl;
-                if (m < g.M) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int p = a0 + row0 + e;
-                        int y = p / g.Wx;
-                        const int x = p - y * g.Wx, n = y / g.Ho;
-                        y -= n * g.Ho;
-                        if (n < g.N && x < g.Wo) out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, vv[e]);
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    const int p = a0 + row0 + e;
+                    int y = p / g.Wx;
+                    const int x = p - y * g.Wx, n = y / g.Ho;
+                    y -= n * g.Ho;
+                    if (n < g.N && x < g.Wo) out_store(g.po, g.O, ((int64_t)n * g.M + m) * plane + y * g.Wo + x, vv[e]);
                 }
             }
         }
@@ -467,9 +507,12 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N
     int ns = (kGmSmemMax - 1024 - 256) / p.stage_bytes;
     p.stages = ns > kGmMaxStages ? kGmMaxStages : ns;
     p.smem = 1024 + p.stages * p.stage_bytes + 256;
-    if (p.stages < 2 || p.BN * kGmBM * 4 > p.stages * p.stage_bytes) return p;
+    // the partial / transpose tile (plus the workspace slices' rounding) aliases the stages
+    const int ptile = p.modeF ? (p.BN + p.S) * kGmPS * 4 : p.BN * kGmBM * 4;
+    if (p.stages < 2 || ptile > p.stages * p.stage_bytes) return p;
     p.x_bytes = ((size_t)p.Prows * p.Kp * elem + 1023) & ~(size_t)1023;
-    p.w_bytes = p.S > 1 ? (size_t)p.S * tiles * p.BN * kGmBM * 4 : 0;
+    p.w_bytes = p.S > 1 ? (size_t)p.S * tiles * p.BN * (p.modeF ? kGmPS : kGmBM) * 4 : 0;
+
     p.ok = true;
     return p;
 }
@@ -545,10 +588,14 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     const int Ho = (Wy - K) / sd + 1, Wo = (Wx - K) / sd + 1;
     const int Wp = Wo;                                      // compact pixel rows
     const int elem = bf16 ? 2 : 4;
-    uint8_t *ws = static_cast<uint8_t *>(workspace_get(p.x_bytes + p.w_bytes, s));
+    // split-K exchange: the L2 workspace round trip (measured faster than
+    // DSMEM even at S = 4 here: configs[4] BF16 21.6 vs 23.0 us);
+    // B200CONV_GM_DSMEM = 1 exchanges through DSMEM instead
+    const bool dsmem = p.S > 1 && env_override("B200CONV_GM_DSMEM", 0) == 1;
+    uint8_t *ws = static_cast<uint8_t *>(workspace_get(p.x_bytes + (dsmem ? 0 : p.w_bytes), s));
     if (!ws) return cudaErrorNotSupported;
     void *X = ws;
-    float *Wk = p.S > 1 ? reinterpret_cast<float *>(ws + p.x_bytes) : nullptr;
+    float *Wk = p.S > 1 && !dsmem ? reinterpret_cast<float *>(ws + p.x_bytes) : nullptr;
     int64_t Ktot = Ktot0;
     if (fpad) {
         void *Fp = auxbuf_get((size_t)M * p.Kp * elem, s);
@@ -564,8 +611,11 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     if (!encode_2d(&tf, !bf16, F, (uint64_t)Ktot, (uint64_t)M, (uint64_t)Ktot * elem, BK, frows) ||
         !encode_2d(&tx, !bf16, X, (uint64_t)p.Kp, (uint64_t)p.Prows, (uint64_t)p.Kp * elem, BK, xrows))
         return cudaErrorNotSupported;
-    // kernel 1: im2col into the (L2-resident) workspace
+    Im2col<float> im32 = {static_cast<const float *>(I), C, Wx, Wy, K, p.Kp, sd, Wp, Ho * Wp, N * Ho * Wp};
+    Im2col<__nv_bfloat16> im16 = {static_cast<const __nv_bfloat16 *>(I), C, Wx, Wy, K, p.Kp, sd, Wp, Ho * Wp,
+                                  N * Ho * Wp};
     {
+        // kernel 1: im2col into the (L2-resident) workspace
         const int64_t vecs = (int64_t)p.Prows * (p.Kp / (16 / elem));
         int blocks = (int)((vecs + 255) / 256);
         if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
@@ -578,12 +628,9 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
         attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cudaError_t e = bf16 ? cudaLaunchKernelEx(&cfg, im2col_kernel<__nv_bfloat16>,
-                                                  static_cast<const __nv_bfloat16 *>(I), C, Wx, Wy, K, p.Prows,
-                                                  p.Kp, static_cast<__nv_bfloat16 *>(X), sd, Wp, Ho * Wp, N * Ho * Wp)
-                             : cudaLaunchKernelEx(&cfg, im2col_kernel<float>, static_cast<const float *>(I), C, Wx,
-                                                  Wy, K, p.Prows, p.Kp, static_cast<float *>(X), sd, Wp, Ho * Wp,
-                                                  N * Ho * Wp);
+        cudaError_t e = bf16 ? cudaLaunchKernelEx(&cfg, im2col_kernel<__nv_bfloat16>, im16, p.Prows,
+                                                  static_cast<__nv_bfloat16 *>(X))
+                             : cudaLaunchKernelEx(&cfg, im2col_kernel<float>, im32, p.Prows, static_cast<float *>(X));
         if (e != cudaSuccess) return e;
     }
     GmArgs g;
@@ -602,7 +649,8 @@ cudaError_t launch_multi_gemm(const void *I, int C, int Wx, int Wy, const void *
     g.Wk = Wk;
     const CUtensorMap &ta = p.modeF ? tf : tx;
     const CUtensorMap &tb = p.modeF ? tx : tf;
-    if (bf16) return p.modeF ? launch_gemm_bn<false, true>(p, ta, tb, g, s) : launch_gemm_bn<false, false>(p, ta, tb, g, s);
+    if (bf16)
+        return p.modeF ? launch_gemm_bn<false, true>(p, ta, tb, g, s) : launch_gemm_bn<false, false>(p, ta, tb, g, s);
     return p.modeF ? launch_gemm_bn<true, true>(p, ta, tb, g, s) : launch_gemm_bn<true, false>(p, ta, tb, g, s);
 }
 

@@ -289,7 +289,8 @@ TC_PATHS = {
     "gemm": {"B200CONV_GM": "2"},
     "gemm-nosplit": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "1"},
     "gemm-split3": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3"},
-    "gemm-dsmem": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "5", "B200CONV_TC_DSMEM": "1"},
+    "gemm-dsmem": {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "5", "B200CONV_GM_DSMEM": "1"},
+    "gemm-ws": {"B200CONV_GM": "2", "B200CONV_GM_DSMEM": "0"},
 }
 
 
