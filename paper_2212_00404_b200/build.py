@@ -32,19 +32,20 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, diag: bool = False, defines=(), out: str = "") -> str:
     """Build the product library; diag=True builds libb200conv_diag.so instead
     (-DB200CONV_DIAG: timeline stamps and work-skipping switches for the
-    tools/ timeline scripts; never loaded by the product path)."""
-    lib = DIAG_LIB if diag else LIB
-    if not force and not _stale(lib):
+    tools/ timeline scripts; never loaded by the product path).  defines/out:
+    an A/B variant (-D flags) written to `out` (tools/, B200CONV_LIB_PATH)."""
+    lib = out or (DIAG_LIB if diag else LIB)
+    if not force and not out and not _stale(lib):
         return lib
-    objdir = os.path.join(PKG, "build_diag" if diag else "build")
+    objdir = os.path.join(PKG, "build_diag" if diag else "build") if not out else lib + ".objs"
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, *(["-DB200CONV_DIAG"] if diag else []), "-Xptxas", "-v", "-c",
+        cmd = [NVCC, *FLAGS, *(["-DB200CONV_DIAG"] if diag else []), *[f"-D{d}" for d in defines], "-Xptxas", "-v", "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -67,4 +68,8 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, diag="--diag" in sys.argv))
+    # python -m paper_2212_00404_b200.build [--force] [-v] [--diag] [--out PATH -DNAME=V ...]
+    a = sys.argv[1:]
+    out = a[a.index("--out") + 1] if "--out" in a else ""
+    print(build(force="--force" in a, verbose="-v" in a, diag="--diag" in a,
+                defines=[x[2:] for x in a if x.startswith("-D")], out=out))
