@@ -220,6 +220,7 @@ typedef struct {
                           persistent KM-TC (grid_y CTAs, one per SM, walk all tiles; block_x 480) */
     int launches;      /* kernel launches per call: 1, or 2 (split-K through the workspace;
                           cluster_x is then 1 and grid_x is the split count) */
+    int chunk_k;       /* KM-SIMT: k-steps (channels x K x K) per pipeline stage; 0 = other kernels */
 } conv_plan;
 
 B200CONV_API int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out);

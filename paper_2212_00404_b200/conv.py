@@ -42,7 +42,7 @@ class ConvError(RuntimeError):
 class ConvPlan(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in
                 ("kernel", "grid_x", "grid_y", "grid_z", "block_x", "cluster_x", "tile_m",
-                 "tile_n", "smem_bytes", "tma_f", "launches")]
+                 "tile_n", "smem_bytes", "tma_f", "launches", "chunk_k")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

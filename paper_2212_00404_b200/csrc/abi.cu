@@ -422,6 +422,7 @@ int conv_plan_single(int Wx, int Wy, int K, int M, conv_plan *out) {
     int st = check_shape(1, Wx, Wy, K, M);
     if (st) return st;
     if (!out) return CONV_E_NULL;
+    *out = conv_plan{};
     plan_single(Wx, Wy, K, M, out);
     return CONV_OK;
 }
@@ -430,6 +431,7 @@ int conv_plan_multi(int C, int Wx, int Wy, int K, int M, int precision, conv_pla
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (!out) return CONV_E_NULL;
+    *out = conv_plan{};
     if (precision >= CONV_FP32 && precision <= CONV_BF16 && plan_multi_c3(C, Wx, Wy, K, M, out) == 0)
         return CONV_OK;
     switch (precision) {
@@ -513,6 +515,7 @@ int conv_plan_multi_batched(int N, int C, int Wx, int Wy, int K, int M, int prec
     int st = check_shape(C, Wx, Wy, K, M);
     if (st) return st;
     if (!out) return CONV_E_NULL;
+    *out = conv_plan{};
     if (precision == CONV_FP32 && N > 1 && !c3_layer(C, Wx, Wy, K, M)) {
         plan_multi_simt(C, Wx, Wy, K, M, out, 1, N);
         return CONV_OK;
@@ -559,6 +562,7 @@ int conv_single_strided_ex(const float *I, int Wx, int Wy, const float *F, int K
 int conv_plan_multi_strided(int N, int C, int Wx, int Wy, int K, int M, int pad, int stride, int precision,
                             conv_plan *out) {
     if (!out) return CONV_E_NULL;
+    *out = conv_plan{};
     if (N < 1 || stride < 1 || pad < 0 || (int64_t)Wx + 2 * pad > INT_MAX / 2 || (int64_t)Wy + 2 * pad > INT_MAX / 2)
         return CONV_E_SHAPE;
     const int Wxp = Wx + 2 * pad, Wyp = Wy + 2 * pad;

@@ -42,6 +42,10 @@ constexpr bool kUnroll2 = B200CONV_SIMT_UNROLL2;   // (A/B build switch: kq loop
 constexpr int kSimtThreads = 256;              // (BM/8) x (BN/8) threads, 8x8 outputs each
 constexpr int kSimtMaxSplit = 16;              // non-portable cluster size on B200
 constexpr int kSimtMaxSmem = 110 * 1024;       // 2 CTAs per SM
+#ifndef B200CONV_SIMT_FIXED_CK
+#define B200CONV_SIMT_FIXED_CK 1
+#endif
+constexpr bool kSimtFixedCk = B200CONV_SIMT_FIXED_CK;   // (A/B build switch: compile-time 36-k chunks)
 
 // diagnostics (B200CONV_SIMT_DBG=1): per-CTA globaltimer stamps [start, after
 // griddepcontrol.wait, chunk 0 staged, main loop done, end << 8 | smid]
@@ -109,7 +113,12 @@ struct SimtShape {
 // CTA per SM, up to 255 registers).  One barrier per chunk: right after it,
 // the stage chunk c - 1 used — which every thread has finished, as the
 // barrier guarantees — is refilled with chunk c + NST - 1.
-template <int BM, int BN, int TN, bool kTmaF, int NST>
+// kCKP > 0: the chunk's k count is a compile-time constant (the TMA-fed
+// K = 3, 4-channel chunk of every 3x3 bench layer: 36), so every shared-memory
+// operand address in the main loop is one base register plus an immediate
+// (measured: the runtime row stride cost ~14 integer instructions per k-quad,
+// each an issue slot the FFMA2 stream needs)
+template <int BM, int BN, int TN, bool kTmaF, int NST, int kCKP = 0>
 __global__ void __launch_bounds__(kSimtThreads, NST == 2 ? 2 : 1)
 kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ I, int C, int Wx, int Wy,
            const float *__restrict__ F,
@@ -131,7 +140,7 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
     const int Ktot = C * KK;
     const int CK = CB * KK;
 
-    const int CKP = (CK + 3) & ~3;                  // k per chunk, padded to whole 16-B quads
+    const int CKP = kCKP > 0 ? kCKP : (CK + 3) & ~3;   // k per chunk, padded to whole 16-B quads
     // F row stride: RS = 4 mod 32 words (cp.async rows); TMA boxes land dense
     // (CKP = CK, CK / 4 not a multiple of 4: consecutive rows still hit
     // different 16-B bank quads)
@@ -550,6 +559,7 @@ void fill_plan(const SimtCfg &c, int C, int Wx, int Wy, int K, int M, conv_plan 
     p->smem_bytes = c.smem;
     p->tma_f = 0;
     p->launches = c.ws ? 2 : 1;
+    p->chunk_k = c.CB * K * K;
     (void)C;
 }
 }  // namespace
@@ -597,7 +607,9 @@ static cudaError_t launch_kms(const SimtCfg &c, const conv_plan &p, const float 
     // the deeper one-CTA-per-SM rings exist for the TMA-fed variant only
     auto kern = !tma ? kms_kernel<BM, BN, TN, false, 2>
                      : c.nst == 3 ? kms_kernel<BM, BN, TN, true, 3>
-                     : c.nst == 4 ? kms_kernel<BM, BN, TN, true, 4> : kms_kernel<BM, BN, TN, true, 2>;
+                     : c.nst == 4 ? kms_kernel<BM, BN, TN, true, 4>
+                     : (c.CB * K * K == 36 && kSimtFixedCk) ? kms_kernel<BM, BN, TN, true, 2, 36>
+                                                            : kms_kernel<BM, BN, TN, true, 2>;
     cudaError_t e = ensure_smem((const void *)kern, p.smem_bytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
