@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False, define
     lib = out or (DIAG_LIB if diag else LIB)
     if not force and not out and not _stale(lib):
         return lib
-    objdir = os.path.join(PKG, "build_diag" if diag else "build") if not out else lib + ".objs"
+    objdir = os.path.join(PKG, "build_diag" if diag else "build") if not out else "/tmp/b200ab_" + os.path.basename(lib) + ".objs"
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):

@@ -46,6 +46,13 @@ constexpr int kSimtMaxSmem = 110 * 1024;       // 2 CTAs per SM
 #define B200CONV_SIMT_FIXED_CK 1
 #endif
 constexpr bool kSimtFixedCk = B200CONV_SIMT_FIXED_CK;   // (A/B build switch: compile-time 36-k chunks)
+#ifndef B200CONV_SIMT_FIXED_UNROLL
+#define B200CONV_SIMT_FIXED_UNROLL 9
+#endif
+// k-quad unroll of the fixed-chunk loop: all 9 (every operand address an
+// immediate off two per-chunk bases; measured configs[4] 124.9 -> 114.4 us
+// against no unroll, 119.2 us with 3)
+constexpr int kSimtFixedUnroll = B200CONV_SIMT_FIXED_UNROLL;
 
 // diagnostics (B200CONV_SIMT_DBG=1): per-CTA globaltimer stamps [start, after
 // griddepcontrol.wait, chunk 0 staged, main loop done, end << 8 | smid]
@@ -290,7 +297,7 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
         const float *Bs2 = Bst + st * CKP * BN + SH::R1 + tn * T2;
         // (kq unrolled by two where it measured faster: TN = 4 and the
         // BM <= 128 TN = 6 tiles, -2..-7 %; the 256 x 48 tile +0.5 %)
-#pragma unroll(NST >= 3 || kUnroll2 || TN == 4 || (TN == 6 && BM <= 128) ? 2 : 1)
+#pragma unroll(kCKP > 0 ? kSimtFixedUnroll : (NST >= 3 || kUnroll2 || TN == 4 || (TN == 6 && BM <= 128) ? 2 : 1))
         for (int kq = 0; kq < CKP; kq += 4) {
             float4 a[8];
 #pragma unroll
