@@ -163,15 +163,20 @@ kms_kernel(const __grid_constant__ CUtensorMap tmapF, const float *__restrict__ 
     const int split = blockIdx.x;
     const int p0 = blockIdx.y * BN;
     const int m0 = blockIdx.z * BM;
-    const int ch_begin = split * ch_per_split;
-    const int ch_end = min(C, ch_begin + ch_per_split);
+    // the ceil(C / CB) channel chunks dealt to the S splits as evenly as whole
+    // chunks allow (sizes differ by at most one chunk; the host's ch_per_split
+    // is the largest share, ceil-rounded, used only for planning)
+    (void)ch_per_split;
+    const int nch_all = (C + CB - 1) / CB;
+    const int ch_begin = (int)((int64_t)split * nch_all / S) * CB;
+    const int ch_end = min(C, (int)((int64_t)(split + 1) * nch_all / S) * CB);
     const int nchunks = ch_end > ch_begin ? (ch_end - ch_begin + CB - 1) / CB : 0;
     const int tid = threadIdx.x;
     const int tn = tid % TNG, tm = tid / TNG;
     // widest copy of F rows (16, 8 or 4 B) that keeps every row start of every
     // chunk aligned
     auto fits = [&](int w) {
-        return (Ktot % w) == 0 && (CK % w) == 0 && ((ch_per_split * KK) % w) == 0 &&
+        return (Ktot % w) == 0 && (CK % w) == 0 &&
                (reinterpret_cast<uintptr_t>(F) % (4 * w)) == 0;
     };
     const int vw = fits(4) ? 4 : (fits(2) ? 2 : 1);

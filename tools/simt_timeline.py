@@ -35,3 +35,8 @@ for want in sys.argv[1:]:
         print(f"== {c['label']} plan {p} CTAs {G} (pctl 0/50/90/100, us)")
         for k, name in enumerate(["start", "pdl-wait", "chunk0", "loop done", "end"]):
             print(f"  {name:10s}", " ".join(f"{v:6.2f}" for v in np.percentile(r[:, k], [0, 50, 90, 100])))
+        S = p["grid_x"]
+        for sp in range(S):
+            rs = r[np.arange(len(r)) % S == sp]
+            print(f"  split {sp}: start {np.percentile(rs[:, 0], 50):6.2f}  chunk0 {np.percentile(rs[:, 2], 50):6.2f}  "
+                  f"loop done p0/50/100 " + " ".join(f"{v:6.2f}" for v in np.percentile(rs[:, 3], [0, 50, 100])))
