@@ -109,18 +109,39 @@ struct GmArgs {
 // floats, filter rows contiguous (the 4-float pad keeps both the row-per-lane
 // writes from TMEM and the pixel-per-lane float4 reads conflict-free).
 constexpr int kGmPS = kGmBM + 4;
+#ifndef B200CONV_GM_OWN_GRAIN
+#define B200CONV_GM_OWN_GRAIN 8
+#endif
+constexpr int kGmOwnGrain = B200CONV_GM_OWN_GRAIN;   // split-K rank pixel ranges: whole groups of this many
 
 // diagnostics (-DB200CONV_DIAG builds, B200CONV_GM_DBG=1): per-CTA globaltimer
 // stamps [start, after griddepcontrol.wait, first stage full (MMA warp),
-// MMAs done (epilogue), epilogue done, cluster barrier passed, end << 8 | smid]
+// MMAs done (epilogue), partial stored (workspace split), cluster barrier
+// passed, end << 8 | smid, partial slices loaded (workspace split)]
 __device__ unsigned long long g_gm_cta[8 * 1024];
+__device__ unsigned long long g_gm_loop[8 * 1024];   // clock64 at each store-loop iteration (thread 0)
 int gm_read_cta_stamps(unsigned long long *host) {
-    return cudaMemcpyFromSymbol(host, g_gm_cta, sizeof(g_gm_cta)) == cudaSuccess ? 0 : 1;
+    return cudaMemcpyFromSymbol(host, g_gm_cta, sizeof(g_gm_cta)) == cudaSuccess &&
+                   cudaMemcpyFromSymbol(host + 8 * 1024, g_gm_loop, sizeof(g_gm_loop)) == cudaSuccess
+               ? 0 : 1;
 }
 __device__ __forceinline__ unsigned long long gm_gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Rank-ordered sum of the S partial tiles' float4 at local_addr across the
+// cluster (DSMEM).  Out of line: the epilogue runs once per CTA, so its code
+// is fetched cold; keeping the loop body small keeps that fetch short.
+__device__ __noinline__ float4 gm_dsmem_sum(uint32_t local_addr, int S) {
+    float4 v = ld_dsmem_f32x4(mapa_shared(local_addr, 0u));
+#pragma unroll 1
+    for (int t = 1; t < S; ++t) {
+        const float4 u = ld_dsmem_f32x4(mapa_shared(local_addr, (uint32_t)t));
+        v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+    }
+    return v;
 }
 
 template <bool kTF32, int BN, bool kModeF>
@@ -264,15 +285,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         tc_fence_before();
     }
     __syncthreads();
-    if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 4] = gm_gtimer();
 
     if constexpr (kModeF) {
         // ---------------------------------------------- store / split-K reduction
         // rank `split` owns pixels [nlo, nhi) of the tile (all S ranks' partials
         // summed in rank order: deterministic); threads run along pixels, so
-        // each of the four filter rows a thread stores is a coalesced warp store
+        // each of the four filter rows a thread stores is a coalesced warp
+        // store.  The ranges are whole 8-pixel groups: every 8 lanes write one
+        // full 32-B sector (a sector written in parts costs a DRAM
+        // read-modify-write; measured configs[4] BF16: the O stores took
+        // ~8 us of the call with 36-pixel ranges)
         const int plane = g.Ho * g.Wo;
-        const int nlo = split * BN / S, nhi = (split + 1) * BN / S, np = nhi - nlo;
+        constexpr int G = kGmOwnGrain;
+        const int nlo = (split * (BN / G) / S) * G;
+        const int nhi = split == S - 1 ? BN : ((split + 1) * (BN / G) / S) * G, np = nhi - nlo;
         const float *src = P;                         // [.][kGmPS] rows of pixel nlo.. (local / workspace)
         int src_p0 = 0;
         if (S > 1 && g.Wk) {
@@ -282,6 +308,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 bulk_commit();
                 bulk_wait<0>();
                 fence_proxy_async_global();
+                if (tl) g_gm_cta[8 * cta_lin + 4] = gm_gtimer();
             }
             cluster_sync_all();
             if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 5] = gm_gtimer();
@@ -290,39 +317,71 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const float *wt = g.Wk + ((int64_t)tile_lin * BN + nlo) * kGmPS;
                 const uint32_t bytes = (uint32_t)(np * kGmPS * 4);
                 mbar_arrive_expect_tx(red_bar, bytes * S);
-                for (int t = 0; t < S; ++t) bulk_load(P + t * np * kGmPS, wt + t * wslice, bytes, red_bar);
+                if (np > 0)
+                    for (int t = 0; t < S; ++t) bulk_load(P + t * np * kGmPS, wt + t * wslice, bytes, red_bar);
             }
             mbar_wait(red_bar, 0);
+            if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 7] = gm_gtimer();
             src_p0 = nlo;
         } else if (S > 1) {
             cluster_sync_all();                       // every rank's partial is in its smem
             if (tl && threadIdx.x == 0) g_gm_cta[8 * cta_lin + 5] = gm_gtimer();
         }
         const uint32_t Pbase = smem_u32(P);
-        for (int idx = threadIdx.x; idx < np * (kGmBM / 4); idx += kGmThreads) {
-            const int qd = idx / np, p = nlo + (idx - qd * np);
-            const int m0 = a0 + 4 * qd;
-            float4 v;
-            if (S > 1 && g.Wk) {
-                const float *sl = src + (p - src_p0) * kGmPS + 4 * qd;
-                v = *reinterpret_cast<const float4 *>(sl);
-                for (int t = 1; t < S; ++t) {
-                    const float4 u = *reinterpret_cast<const float4 *>(sl + t * np * kGmPS);
-                    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
-                }
-            } else if (S > 1) {
-                v = dsmem_sum_ranks<kGmMaxSplit>(Pbase + (uint32_t)((p * kGmPS + 4 * qd) * 4), S);
-            } else {
-                v = *reinterpret_cast<const float4 *>(P + p * kGmPS + 4 * qd);
-            }
-            const int pg = b0 + p;                    // compact pixel over all images
-            const int n = pg / plane;
-            if (n < g.N) {
-                const int64_t o = ((int64_t)n * g.M + m0) * plane + (pg - n * plane);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
+        // items (filter quad qd, pixel p) dealt round-robin to the threads,
+        // four per thread per batch: all their shared-memory loads issue
+        // before the sums and stores (the loop ran once per CTA, latency-bound
+        // at ~700 clk per item with one item in flight); item indices advance
+        // without divisions
+        const int total = np * (kGmBM / 4);
+        int qd = np > 0 ? (int)threadIdx.x / np : 0, pp = (int)threadIdx.x - qd * np;
+        const int dq = np > 0 ? kGmThreads / np : 0, dp = kGmThreads - dq * np;
+        int it_dbg = 0;
+        for (int idx0 = threadIdx.x; idx0 < ((kDiag && (g.dbg & 4)) ? 0 : total); idx0 += 4 * kGmThreads) {
+            if (tl && threadIdx.x == 0 && it_dbg < 8) g_gm_loop[8 * cta_lin + it_dbg++] = clock64();
+            float4 v[4];
+            int qv[4], pv[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (m0 + e < g.M) out_store(g.po, g.O, o + (int64_t)e * plane, vv[e]);
+            for (int u = 0; u < 4; ++u) {
+                qv[u] = qd;
+                pv[u] = nlo + pp;
+                if (idx0 + u * kGmThreads < total) {
+                    if (S > 1 && g.Wk) {
+                        const float *sl = src + (pv[u] - src_p0) * kGmPS + 4 * qd;
+                        v[u] = *reinterpret_cast<const float4 *>(sl);
+#pragma unroll 4
+                        for (int t = 1; t < S; ++t) {
+                            const float4 w = *reinterpret_cast<const float4 *>(sl + t * np * kGmPS);
+                            v[u].x += w.x; v[u].y += w.y; v[u].z += w.z; v[u].w += w.w;
+                        }
+                    } else if (S > 1) {
+                        v[u] = gm_dsmem_sum(Pbase + (uint32_t)((pv[u] * kGmPS + 4 * qd) * 4), S);
+                    } else {
+                        v[u] = *reinterpret_cast<const float4 *>(P + pv[u] * kGmPS + 4 * qd);
+                    }
+                }
+                pp += dp;
+                qd += dq;
+                if (pp >= np) { pp -= np; ++qd; }
+            }
+            if (kDiag && (g.dbg & 2)) continue;       // (diag: no O stores)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (idx0 + u * kGmThreads >= total) break;
+                const int m0 = a0 + 4 * qv[u];
+                const int pg = b0 + pv[u];            // compact pixel over all images
+                const int n = g.N > 1 ? pg / plane : (pg < plane ? 0 : 1);   // rows past the map: n = N
+                if (n >= g.N) continue;
+                const int64_t o = ((int64_t)n * g.M + m0) * plane + (pg - n * plane);
+                const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                if (!g.po.mc && g.po.n == 0 && m0 + 3 < g.M) {
+                    float *op = g.O + o;
+                    op[0] = vv[0]; op[plane] = vv[1]; op[2 * plane] = vv[2]; op[3 * plane] = vv[3];
+                } else {
+#pragma unroll 1
+                    for (int e = 0; e < 4; ++e)
+                        if (m0 + e < g.M) out_store(g.po, g.O, o + (int64_t)e * plane, vv[e]);
+                }
             }
         }
         if (S > 1 && !g.Wk) cluster_sync_all();      // keep this CTA's partial alive for the others
@@ -508,7 +567,7 @@ GmPlan gm_plan(int C, int Wx, int Wy, int K, int M, bool bf16, int sd = 1, int N
     p.stages = ns > kGmMaxStages ? kGmMaxStages : ns;
     p.smem = 1024 + p.stages * p.stage_bytes + 256;
     // the partial / transpose tile (plus the workspace slices' rounding) aliases the stages
-    const int ptile = p.modeF ? (p.BN + p.S) * kGmPS * 4 : p.BN * kGmBM * 4;
+    const int ptile = p.modeF ? (p.BN + kGmOwnGrain * p.S) * kGmPS * 4 : p.BN * kGmBM * 4;
     if (p.stages < 2 || ptile > p.stages * p.stage_bytes) return p;
     p.x_bytes = ((size_t)p.Prows * p.Kp * elem + 1023) & ~(size_t)1023;
     p.w_bytes = p.S > 1 ? (size_t)p.S * tiles * p.BN * (p.modeF ? kGmPS : kGmBM) * 4 : 0;

@@ -21,7 +21,7 @@ for want in sys.argv[1:]:
         call = lambda j: conv.conv_multi_ex(I, c["C"], c["Wx"], c["Wy"], Fs[j % 4], c["K"], c["M"], Os[j % 4], c["prec"])
         for j in range(4): call(j)
         torch.cuda.synchronize()
-        os.environ["B200CONV_GM_DBG"] = "1"
+        os.environ["B200CONV_GM_DBG"] = os.environ.get("DBG", "1")
         for j in range(4): call(j)
         torch.cuda.synchronize()
         os.environ.pop("B200CONV_GM_DBG")
@@ -30,16 +30,20 @@ for want in sys.argv[1:]:
             print(c["label"], "is not on KM-TC/G", p)
             continue
         G = p["grid_x"] * p["grid_y"] * p["grid_z"]
-        buf = (ctypes.c_ulonglong * 8192)()
+        buf = (ctypes.c_ulonglong * 16384)()
         lib.conv_diag_gm_cta_stamps(buf)
-        tu = np.array(list(buf), dtype=np.uint64).reshape(1024, 8)[:min(G, 1024)]
+        allb = np.array(list(buf), dtype=np.uint64)
+        tu = allb[:8192].reshape(1024, 8)[:min(G, 1024)]
+        lp = allb[8192:].reshape(1024, 8)[:min(G, 1024)].astype(np.int64)
         end = (tu[:, 6] >> np.uint64(8)) | (tu[:, 0] & ~np.uint64((1 << 56) - 1))
         t = tu.astype(np.int64)
         t[:, 6] = end.astype(np.int64)
         t[:, 5] = np.where(t[:, 5] == 0, t[:, 4], t[:, 5])
         r = (t - t[:, 0].min()) / 1e3
         print(f"== {c['label']} plan {p} CTAs {G} (percentiles 0/50/90/100 of us since the first CTA start)")
-        for k, name in [(0, "start"), (1, "pdl-wait"), (2, "stage0 full"), (3, "mma done"), (4, "epilogue"),
-                        (5, "cluster sync"), (6, "end")]:
+        for k, name in [(0, "start"), (1, "pdl-wait"), (2, "stage0 full"), (3, "mma done"), (4, "partial stored"),
+                        (5, "cluster sync"), (7, "slices loaded"), (6, "end")]:
             v = r[:, k]
             print(f"  {name:14s} " + " ".join(f"{np.percentile(v, q):7.2f}" for q in (0, 50, 90, 100)))
+        d = np.diff(lp, axis=1)
+        print("  store-loop clock64 deltas per iteration (median over CTAs):", np.median(d, axis=0))
