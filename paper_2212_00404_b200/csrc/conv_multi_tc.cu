@@ -132,6 +132,19 @@ __device__ __forceinline__ unsigned long long tc_gtimer() {
     return t;
 }
 
+// Rank-ordered sum of the S partial tiles' float4 at local_addr across the
+// cluster (DSMEM); out of line, so the once-per-CTA reduction loop stays small
+// (its code is fetched cold).
+__device__ __noinline__ float4 tc_dsmem_sum(uint32_t local_addr, int S) {
+    float4 v = ld_dsmem_f32x4(mapa_shared(local_addr, 0u));
+#pragma unroll 1
+    for (int t = 1; t < S; ++t) {
+        const float4 u = ld_dsmem_f32x4(mapa_shared(local_addr, (uint32_t)t));
+        v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+    }
+    return v;
+}
+
 template <bool kTF32, int BN, bool kTmaB, bool kPatch>
 __global__ void __launch_bounds__(kTcThreads, 1)
 kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapI,
@@ -525,30 +538,70 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
             mbar_wait(red_bar, 0);
             if (tl && threadIdx.x == 0) g_tc_cta[8 * cta_lin + 7] = tc_gtimer();
         }
-        for (int idx = threadIdx.x; idx < rows * (kTcBM / 4); idx += kTcThreads) {
-            const int nl = nlo + idx / (kTcBM / 4), row0 = 4 * (idx % (kTcBM / 4));
-            const uint32_t off = (uint32_t)((nl * kTcBM + row0) * 4);
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (dbg & 512) {
-            } else if (Wk) {
-                const float *sl = slices + (nl - nlo) * kTcBM + row0;
-                v = *reinterpret_cast<const float4 *>(sl);
-                for (int t = 1; t < S; ++t) {
-                    const float4 u = *reinterpret_cast<const float4 *>(sl + t * rows * kTcBM);
-                    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
-                }
-            } else {
-                v = dsmem_sum_ranks<kTcMaxSplit>(Pbase + off, S);
-            }
-            const int m = n0 + nl;
-            if (m < M && !(dbg & 1024)) {
-                const float vv[4] = {v.x, v.y, v.z, v.w};
+        // thread -> 4 fixed pixels (row0 = 4 * lane) and filter rows lane-warp
+        // + kTcWarps * j; four rows per batch, every partial load of a batch
+        // in flight before the sums and stores (this loop runs once per CTA:
+        // one item at a time it was latency-bound, ~6 us on configs[4] TF32)
+        constexpr int kTcWarps = kTcThreads / 32;
+        const int row0 = 4 * (int)lane;
+        int64_t opix[4];
+        bool pvalid[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int pe = p0 + row0 + e;
-                    const int y = pe / Wx, x = pe - y * Wx;
-                    if (pe < Ho * Wx && x < Wo) O[(int64_t)m * plane + (int64_t)y * Wo + x] = vv[e];
+        for (int e = 0; e < 4; ++e) {
+            const int pe = p0 + row0 + e;
+            const int y = pe / Wx, x = pe - y * Wx;
+            pvalid[e] = pe < Ho * Wx && x < Wo;
+            opix[e] = (int64_t)y * Wo + x;
+        }
+        for (int nb = (int)warp; nb < rows; nb += 4 * kTcWarps) {
+            float4 v[4];
+            if (!Wk && S <= 4 && !(dbg & 512)) {
+                // DSMEM, up to 4 ranks: all 16 remote loads of the batch first
+                float4 w[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (t < S && nb + u * kTcWarps < rows)
+                            w[u][t] = ld_dsmem_f32x4(mapa_shared(
+                                Pbase + (uint32_t)(((nlo + nb + u * kTcWarps) * kTcBM + row0) * 4), (uint32_t)t));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    v[u] = w[u][0];                      // rank order: 0, 1, ..., S-1
+#pragma unroll
+                    for (int t = 1; t < 4; ++t)
+                        if (t < S && nb + u * kTcWarps < rows) {
+                            v[u].x += w[u][t].x; v[u].y += w[u][t].y; v[u].z += w[u][t].z; v[u].w += w[u][t].w;
+                        }
                 }
+            } else
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int nl = nlo + nb + u * kTcWarps;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (nb + u * kTcWarps >= rows || (dbg & 512)) continue;
+                if (Wk) {
+                    const float *sl = slices + (nl - nlo) * kTcBM + row0;
+                    v[u] = *reinterpret_cast<const float4 *>(sl);
+#pragma unroll 4
+                    for (int t = 1; t < S; ++t) {
+                        const float4 w = *reinterpret_cast<const float4 *>(sl + t * rows * kTcBM);
+                        v[u].x += w.x; v[u].y += w.y; v[u].z += w.z; v[u].w += w.w;
+                    }
+                } else {
+                    v[u] = tc_dsmem_sum(Pbase + (uint32_t)((nl * kTcBM + row0) * 4), S);
+                }
+            }
+            if (dbg & 1024) continue;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = n0 + nlo + nb + u * kTcWarps;
+                if (nb + u * kTcWarps >= rows || m >= M) continue;
+                float *o = O + (int64_t)m * plane;
+                if (pvalid[0]) o[opix[0]] = v[u].x;
+                if (pvalid[1]) o[opix[1]] = v[u].y;
+                if (pvalid[2]) o[opix[2]] = v[u].z;
+                if (pvalid[3]) o[opix[3]] = v[u].w;
             }
         }
         if (!Wk) cluster_sync_all();          // keep this CTA's partial alive for the others
