@@ -71,6 +71,7 @@ for prec in ("fp32", "tf32", "bf16"):
 multi(32, 14, 3, 48, "fp32", {"B200CONV_SIMT_FORCE": "0,1,0"}, name="KM-SIMT nosplit")
 multi(32, 14, 3, 48, "fp32", {"B200CONV_SIMT_FORCE": "3,4,0"}, name="KM-SIMT cluster")
 multi(32, 14, 3, 48, "fp32", {"B200CONV_SIMT_FORCE": "7,5,1"}, name="KM-SIMT workspace")
+multi(64, 14, 3, 256, "fp32", {"B200CONV_SIMT_FORCE": "3,4,1"}, name="KM-SIMT 256x48 fixed-36 workspace")
 multi(13, 11, 3, 21, "fp32", name="KM-SIMT odd (cp.async F)")
 multi(16, 12, 3, 40, "fp32", N=3, name="KM-SIMT batch")
 multi(16, 15, 3, 24, "fp32", N=2, pad=1, stride=2, name="KM-SIMT strided")
@@ -83,6 +84,9 @@ for prec in ("tf32", "bf16"):
     multi(64, 28, 3, 64, prec, N=40, name="KM-TC persistent batch")
     multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2"}, name="KM-TC/G")
     multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3"}, name="KM-TC/G split")
+    multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3", "B200CONV_GM_DSMEM": "1"},
+          name="KM-TC/G split DSMEM")
+    multi(64, 14, 3, 512, prec, {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "4"}, name="KM-TC/G 144-px split")
     multi(3, 20, 3, 16, prec, N=2, pad=1, stride=2, name="KM-TC/G strided (pad rows)")
     multi(32, 9, 3, 40, prec, N=2, pad=1, name="KM-TC padded")
 print("FAILS", fails)
