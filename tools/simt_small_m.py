@@ -1,5 +1,5 @@
 """KM-SIMT forced configurations on the configs[4] shard of M filters:
-usage: simt_small_m.py M "tile,S,ws;..." """
+usage: simt_small_m.py M "tile,S,ws[/NST];..." """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
@@ -32,10 +32,12 @@ def timeit(fn, reps=20):
 
 out = []
 for v in [""] + sys.argv[2].split(";"):
-    if v:
-        os.environ["B200CONV_SIMT_FORCE"] = v
-    else:
-        os.environ.pop("B200CONV_SIMT_FORCE", None)
+    force, _, nst = v.partition("/")          # "tile,S,ws[/NST]"
+    for k, x in (("B200CONV_SIMT_FORCE", force), ("B200CONV_SIMT_NST", nst)):
+        if x:
+            os.environ[k] = x
+        else:
+            os.environ.pop(k, None)
     p = conv.plan_multi(C, W, W, K, M, "fp32")
     us = timeit(lambda j: conv.conv_multi_ex(I, C, W, W, Fs[j % 4], K, M, Os[j % 4], "fp32", s.cuda_stream))
     out.append(f"{v or 'planner'}[{p['tile_m']}x{p['tile_n']} S{p['grid_x']} L{p['launches']}]: {us:.2f}")

@@ -52,7 +52,9 @@ def time_cfg(I, F, O, L, reps=20):
 
 
 out = []
-for L in synth.MULTI_LAYERS + [synth.SHARD_SWEEP]:
+# the per-rank shards of the strong-scaled configs[4] sweep (M / G filters, G = 2, 4, 8)
+SHARDS = [dict(synth.SHARD_SWEEP, name=f"shard{g}_14x14_c512_m{4096 // g}_k3", M=4096 // g) for g in (2, 4, 8)]
+for L in synth.MULTI_LAYERS + [synth.SHARD_SWEEP] + SHARDS:
     if want not in L["name"]:
         continue
     I = torch.from_numpy(synth.uniform01(synth.SEED_I, (L["C"], L["Wy"], L["Wx"]))).to(dev)
