@@ -50,5 +50,9 @@ for G in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
 
     one = {p: timeit(lambda j, p=p: call(p, j)) for p in bufs}
     step = timeit(lambda j: [call(p, j) for p in bufs])
+    if os.environ.get("ORDERS"):
+        import itertools
+        for order in itertools.permutations(bufs):
+            print(f"  order {'>'.join(order)}: {timeit(lambda j: [call(p, j) for p in order]):7.2f} us", flush=True)
     print(f"G={G} M={M}: step {step:7.2f} us | " + " | ".join(f"{p} {one[p]:7.2f}" for p in one) +
           f" | plans " + " ".join(str(conv.plan_multi(C, W, W, K, M, p)["kernel"]) for p in bufs), flush=True)
