@@ -68,6 +68,9 @@
  *   B200CONV_PLANNER=paper  KS row blocks by the paper's N_FMA rule instead
  *                           of the measured row threshold (NEXT-4 A/B)
  *   B200CONV_SIMT_NST=2..4  KM-SIMT ring depth (3, 4: one CTA per SM)
+ *   B200CONV_KS_FLAT=0|1    KS-L (line-aligned flat chunks for K = 3 maps whose
+ *                           output rows are not whole 128-B lines) off | used
+ *                           wherever legal (default: Ho >= 128, M >= 256)
  * Timeline stamps and work-skipping diagnostics exist only in the separate
  * -DB200CONV_DIAG build (libb200conv_diag.so), never in this library.
  *

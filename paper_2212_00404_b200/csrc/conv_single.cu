@@ -366,6 +366,126 @@ ks_kernel(const KsArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- KS-L: line-aligned flat units
+// K = 3 maps whose output rows are not whole 128-B lines (Wo % 32 != 0, e.g.
+// 224x224 -> 222 = 888-B rows): the row-block units above cut every row into
+// 32-lane pieces that start mid-line, so each piece boundary's line is written
+// by two warp stores (measured 1.51x L2 write requests and 13.95 vs 10.82 us
+// against the 16-B/128-B aligned 226x226 map, profiles/ks_alignment_r02.txt).
+// Here a unit is one 128-B-aligned 64-float chunk of ONE filter plane's flat
+// output (rows run on into the next row): lane l computes the pixel pair at
+// flat p = h + 64 (c - 1) + 2 l for four filters, so each of its four warp
+// stores writes exactly two whole lines.  The four filters of a lane are
+// m, m + P, m + 2P, m + 3P, where P is the alignment period of the planes
+// (P * Ho * Wo == 0 mod 32 floats): they share the line offset h of their
+// planes, so one pixel mapping is aligned for all four.  Rows of the pair
+// never split (Wo even, p even).  The CTA owns a contiguous chunk range of one
+// filter group and stages the input rows those chunks need.
+struct KfArgs {
+    const float *I;
+    const float *F;
+    float *O;
+    int Wx, Wy, M;
+    int P;        // plane alignment period (filters)
+    int NG;       // filter groups: ceil(M / (4P)) * P
+    int nch;      // 64-float chunks per plane (incl. the partial head chunk)
+    int nsplit;   // CTAs per filter group (contiguous chunk ranges)
+};
+
+__global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) {
+    constexpr int K = 3, R = 4;
+    extern __shared__ __align__(16) float smem[];
+    const int Wx = a.Wx, Wy = a.Wy, M = a.M, P = a.P;
+    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
+    const int HW = Ho * Wo;
+    const int64_t plane = HW;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // CTA -> (filter group, contiguous chunk range); warp -> an eighth of it.
+    // Each warp writes long contiguous ranges of its four planes.
+    const int g = blockIdx.x / a.nsplit, sp = blockIdx.x - g * a.nsplit;
+    const int cs0 = (int)((int64_t)sp * a.nch / a.nsplit), cs1 = (int)((int64_t)(sp + 1) * a.nch / a.nsplit);
+    const int wc0 = cs0 + (int)((int64_t)warp * (cs1 - cs0) / kKsWarps);
+    const int wc1 = cs0 + (int)((int64_t)(warp + 1) * (cs1 - cs0) / kKsWarps);
+    const int gb = g / P, r = g - gb * P;
+    const int h = (32 - (int)(((int64_t)r * (plane & 31)) & 31)) & 31;   // first line-aligned p of these planes
+    const int m0 = gb * P * R + r;
+    // taps of the four filters, [t][f] (FFMA2 pairs along filters)
+    float w[9 * R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int m = m0 + P * i;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) w[t * R + i] = 0.f;
+        if (m < M) {
+#pragma unroll
+            for (int t = 0; t < 9; ++t) w[t * R + i] = __ldg(a.F + (int64_t)m * 9 + t);
+        }
+    }
+    // the CTA stages the input rows of its chunk range (measured faster than
+    // per-warp row ranges: 12.7 vs 13.2 us on 224x224 M=256)
+    const int p_lo = max(0, h + 64 * (cs0 - 1)), p_hi = min(HW - 1, h + 64 * cs1 - 1);
+    const int row_lo = p_lo / Wo, row_hi = min(Wy, p_hi / Wo + K);
+    const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
+    const int pad = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3);
+    pdl_wait();
+    {
+        const int n16 = (int)((pad + (e1 - e0) + 3) >> 2);
+        for (int c = tid; c < n16; c += kKsThreads) {
+            const int64_t e = e0 - pad + 4 * c;
+            if (e >= e0 && e + 4 <= e1) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             ::"r"(smem_u32(smem + 4 * c)), "l"(a.I + e) : "memory");
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool ok = e + i >= e0 && e + i < e1;
+                    cp_async4(smem + 4 * c + i, ok ? a.I + e + i : a.I, ok);
+                }
+            }
+        }
+    }
+    cp_async_commit();
+    pdl_trigger();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (wc0 >= wc1) return;
+    const float *sin = smem + pad - e0;                  // sin[y*Wx + x] = I[y][x]
+    float *O0 = a.O + (int64_t)m0 * plane;
+    int p = h + 64 * (wc0 - 1) + 2 * lane;
+    int y = 0, x = p;
+    if (p >= 0) { y = p / Wo; x = p - y * Wo; }
+    for (int c = wc0; c < wc1; ++c) {
+        const bool valid = p >= 0 && p < HW;
+        const float *base = sin + (valid ? (int64_t)y * Wx + x : e0);
+        float acc[R][2];
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[i][0] = acc[i][1] = 0.f;
+#pragma unroll
+        for (int rr = 0; rr < K; ++rr) {
+            float win[4];
+            lds_vec<2>(base + rr * Wx, win);
+            lds_vec<2>(base + rr * Wx + 2, win + 2);
+#pragma unroll
+            for (int cc = 0; cc < K; ++cc) {
+                const int t = rr * K + cc;
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    ffma2(acc[0][v], acc[1][v], win[v + cc], w[t * R], w[t * R + 1]);
+                    ffma2(acc[2][v], acc[3][v], win[v + cc], w[t * R + 2], w[t * R + 3]);
+                }
+            }
+        }
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (m0 + P * i < M) stg_vec<2>(O0 + (int64_t)P * i * plane + p, acc[i]);
+        }
+        p += 64;
+        x += 64;
+        while (x >= Wo) { x -= Wo; ++y; }
+    }
+}
+
 // Generic fallback (any K, e.g. K = Wx = Wy, or rows too wide for smem): no
 // staging, loads through L1.
 template <int R, int TY>
@@ -533,12 +653,65 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
 }
 }  // namespace
 
+// KS-L plan (K = 3 maps with rows that are not whole lines); false when it
+// does not apply.  B200CONV_KS_FLAT=0 disables it, =1 uses it wherever legal.
+static bool plan_ks_flat(const void *I, int Wx, int Wy, int K, int M, const float *O, KfArgs *fa, int *Gout,
+                         int *smem_bytes) {
+    const int v = env_override("B200CONV_KS_FLAT", -1);
+    if (v == 0 || K != 3) return false;
+    const int Wo = Wx - K + 1, Ho = Wy - K + 1;
+    const int64_t HW = (int64_t)Ho * Wo;
+    if (Wo < 2 || Ho < 1 || Wo % 2 != 0 || Wx % 2 != 0 || !al(I, 8) || !al(O, 128)) return false;
+    if (HW + 64 > ((int64_t)1 << 30) / 4) return false;
+    // measured (tools/ks_variants.py): 224x224 M=256 12.7 vs 14.0 us; ties at
+    // M = 128, slower below and on 112-114 px maps (the row-block kernel's
+    // two-row register blocks and 3 CTAs/SM matter more there)
+    if (v != 1 && (Wo % 32 == 0 || Ho < 128 || M < 256)) return false;
+    int gcd = 32, q = (int)(HW & 31);
+    for (int b = q; b != 0;) { const int t = gcd % b; gcd = b; b = t; }
+    const int P = 32 / gcd;
+    KfArgs a = {};
+    a.Wx = Wx; a.Wy = Wy; a.M = M;
+    a.P = P;
+    a.NG = (M + 4 * P - 1) / (4 * P) * P;
+    a.nch = (int)(1 + (HW + 63) / 64);
+    // one wave of 3 CTAs per SM: contiguous chunk ranges per filter group
+    int ns = 3 * num_sms() / a.NG;
+    if (kDiag) ns = env_override("B200CONV_KS_FLAT_NS", ns);
+    if (ns < 1) ns = 1;
+    if (ns > a.nch) ns = a.nch;
+    a.nsplit = ns;
+    const int G = a.NG * ns;
+    // staged rows of the longest CTA range: chunks + head/tail slack, + K - 1
+    const int64_t span = (int64_t)(a.nch + ns - 1) / ns * 64 + 64 + 32;
+    const int64_t rows = span / Wo + 2 + K;
+    const int64_t sm = ((rows < Wy ? rows : Wy) * Wx + 16) * 4;
+    if (sm > 72 * 1024) return false;
+    *fa = a;
+    *Gout = G;
+    *smem_bytes = (int)sm;
+    return true;
+}
+
 int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     p->cluster_x = 1;
     p->tma_f = 0;
     p->launches = 1;
     p->kernel = 0;
+    KfArgs fa;
+    int fg = 0, fsm = 0;
+    if (plan_ks_flat(reinterpret_cast<const float *>(256), Wx, Wy, K, M, reinterpret_cast<float *>(256), &fa, &fg,
+                     &fsm)) {
+        p->block_x = kKsThreads;
+        p->grid_x = fg;
+        p->grid_y = 1;
+        p->grid_z = 1;
+        p->tile_m = 4;                                    // filters per lane (P apart)
+        p->tile_n = -2;                                   // marks KS-L (64-float flat chunks)
+        p->smem_bytes = fsm;
+        return 0;
+    }
     KsPlan kp;
     // plans are computed for 16-B aligned I / O (torch allocations)
     if (plan_ks(reinterpret_cast<const float *>(256), Wx, Wy, nullptr, K, M,
@@ -680,6 +853,23 @@ cudaError_t launch_multi_c3(const void *I, int C, int Wx, int Wy, const void *F,
 
 cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K, int M, float *O,
                           cudaStream_t s) {
+    {
+        KfArgs fa;
+        int G = 0, sm = 0;
+        if (plan_ks_flat(I, Wx, Wy, K, M, O, &fa, &G, &sm)) {
+            fa.I = I; fa.F = F; fa.O = O;
+            if (cudaError_t e = ensure_smem((const void *)ks_flat_kernel, sm); e != cudaSuccess) return e;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(G);
+            cfg.blockDim = dim3(kKsThreads);
+            cfg.dynamicSmemBytes = sm;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1] = {pdl_attr()};
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, ks_flat_kernel, fa);
+        }
+    }
     KsPlan kp;
     if (plan_ks(I, Wx, Wy, F, K, M, O, &kp)) {
         switch (K) {

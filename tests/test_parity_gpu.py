@@ -103,6 +103,26 @@ def test_single_edge_cases(conv, Wx, Wy, K, M):
     assert_parity(run_single(conv, I, F), Oo, A, TAU["fp32"], f"single {Wx}x{Wy} K{K} M{M}")
 
 
+# KS-L (line-aligned flat chunks, conv_single.cu): forced on shapes covering
+# every plane alignment period P (1, 2, 4, 8, 16), filter counts that leave
+# groups partly empty, tiny and ragged maps
+KSL_SHAPES = [(10, 10, 4), (12, 9, 7), (34, 20, 33), (30, 30, 48), (58, 45, 20), (100, 37, 70),
+              (224, 224, 12), (66, 130, 9)]
+
+
+@pytest.mark.parametrize("Wx,Wy,M", KSL_SHAPES)
+def test_single_ksl_forced_matches_oracle(conv, monkeypatch, Wx, Wy, M):
+    monkeypatch.setenv("B200CONV_KS_FLAT", "1")
+    assert conv.plan_single(Wx, Wy, 3, M)["tile_n"] == -2
+    I = synth.uniform01(31, (Wy, Wx))
+    F = synth.uniform_pm1(32, (M, 3, 3))
+    Oo, A = oracle.conv_single(I, F)
+    assert_parity(run_single(conv, I, F), Oo, A, TAU["fp32"], f"KS-L {Wx}x{Wy} M{M}")
+    Ii, Fi = synth.layer_inputs(1, Wx, Wy, 3, M, kind="ints")
+    Oi, _ = oracle.conv_single(Ii[0], Fi[:, 0])
+    assert np.array_equal(run_single(conv, Ii[0], Fi[:, 0]), Oi)
+
+
 def test_single_positive_stress_and_ints(conv):
     I, F = synth.layer_inputs(1, 56, 56, 7, 32, kind="positive")
     Oo, A = oracle.conv_single(I[0], F[:, 0])
