@@ -58,7 +58,10 @@ constexpr uint32_t kMmaWarp = 8 + kTcProducers;   // TMEM allocator + tcgen05.mm
 constexpr int kTcBM = 128;            // pixels per tile (UMMA M)
 constexpr int kTcMaxSplit = 16;      // non-portable cluster size on B200
 constexpr int kTcSmemMax = 225 * 1024;
-constexpr int kTcMaxStages = 8;
+#ifndef B200CONV_TC_MAX_STAGES
+#define B200CONV_TC_MAX_STAGES 8
+#endif
+constexpr int kTcMaxStages = B200CONV_TC_MAX_STAGES;   // (A/B builds: -DB200CONV_TC_MAX_STAGES=12)
 
 template <bool kTF32>
 struct TcTraits {
@@ -83,7 +86,7 @@ struct TcGeom {
     int smem;
 };
 
-__host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool patch) {
+__host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool patch, int extra = 0) {
     TcGeom g;
     const int BK = 128 / elem;
     // a box must start 16-B aligned in global memory: the patch starts up to
@@ -101,10 +104,10 @@ __host__ __device__ inline TcGeom tc_geom(int Wx, int K, int BN, int elem, bool 
     g.stage_bytes = BN * 128 + g.patch_bytes;
     // k -> patch offset table for every phase (k0 mod K*K) of a k-block (K <= 7)
     g.tab_bytes = (patch && K <= 7) ? K * K * BK * 4 : 0;
-    int st = (kTcSmemMax - 1024 - 512 - g.tab_bytes) / g.stage_bytes;
+    int st = (kTcSmemMax - 1024 - 512 - g.tab_bytes - extra) / g.stage_bytes;
     g.stages = st > kTcMaxStages ? kTcMaxStages : st;
     if (g.stages > (512 - BN) / 32) g.stages = (512 - BN) / 32;       // TMEM: BN + 32 * stages <= 512
-    g.smem = 1024 + g.stages * g.stage_bytes + 512 + g.tab_bytes;
+    g.smem = 1024 + g.stages * g.stage_bytes + 512 + g.tab_bytes + extra;
     return g;
 }
 
@@ -627,8 +630,15 @@ kmtc_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ C
 // This removes the per-tile prologue (TMEM alloc, barrier init, descriptor
 // prefetch) and the pipeline fill that the one-tile-per-CTA kernel pays at
 // every tile.
-constexpr int kTpEpiWarp = 8 + kTcProducers + 1;            // warps 11..14: epilogue
-constexpr int kTpThreads = 32 * (kTpEpiWarp + 4);
+#ifndef B200CONV_TP_EPI_GROUPS
+#define B200CONV_TP_EPI_GROUPS 2
+#endif
+constexpr int kTpEpiGroups = B200CONV_TP_EPI_GROUPS;         // epilogue warp groups (4 warps each)
+constexpr int kTpEpiWarp = 8 + kTcProducers + 1;            // warps 11..: epilogue
+constexpr int kTpThreads = 32 * (kTpEpiWarp + 4 * kTpEpiGroups);
+// epilogue staging: per group, 16 filters x 128 pixels of the accumulator,
+// transposed so each filter's outputs leave as one contiguous run of O
+constexpr int kTpEpiBytes = kTpEpiGroups * 16 * kTcBM * 4;
 
 template <bool kTF32, int BN>
 __global__ void __launch_bounds__(kTpThreads, 1)
@@ -642,7 +652,7 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
     const int Ktot = C * KK;
     const int Ho = Wy - K + 1, Wo = (Wv > 0 ? Wv : Wx) - K + 1;   // Wv: see kmtc_kernel
     const int nkb = Ktot / BK;                           // plan: Ktot % BK == 0
-    const TcGeom geo = tc_geom(Wx, K, BN, Tr::kElem, true);
+    const TcGeom geo = tc_geom(Wx, K, BN, Tr::kElem, true, kTpEpiBytes);
     const int NS = geo.stages;
     const int STAGE = geo.stage_bytes;
     const int nft = (M + BN - 1) / BN;
@@ -674,7 +684,7 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 4);                        // 4 epilogue warps
+        mbar_init(tmem_empty, 4 * kTpEpiGroups);         // every epilogue warp
         fence_mbar_init();
         tma_prefetch_desc(&tmapF);
         tma_prefetch_desc(&tmapI);
@@ -687,6 +697,13 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
     pdl_wait();
     pdl_trigger();
 
+    // diagnostic build: clock64 stamps of CTA 0's first 256 ring iterations
+    // (P: producer past empty, G0: gather warp 0 past pfull, G1: its arrive,
+    // M: MMA issuer past full) -> g_tc_stamps, tools/tc_stamp_persist.py
+    const bool pst = kDiag && blockIdx.x == 0;
+    auto pstamp = [&](int slot, int i) {
+        if (pst && i < 256) g_tc_stamps[slot * 256 + i] = (unsigned long long)clock64();
+    };
     auto tile_of = [&](int t, int *p0, int *n0, int *img) {
         const int y = t / nft;
         *n0 = (t - y * nft) * BN;
@@ -709,6 +726,7 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
                     if ((i % kTcProducers) != pw) continue;
                     const int s = i % NS, ph = (i / NS) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
+                    pstamp(0, i);
                     uint8_t *st = smem + s * STAGE;
                     mbar_arrive_expect_tx(&pfull[s], (uint32_t)(geo.pch * geo.pb * Tr::kElem));
                     tma_load_2d(st + B_BYTES, &tmapI, &pfull[s], p0, img * C + ch_lo);
@@ -730,6 +748,7 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
                 for (int kb = 0; kb < nkb; ++kb, ++i) {
                     const int s = i % NS;
                     mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+                    pstamp(3, i);
                     tc_fence_after();
                     const uint32_t b_addr = smem_u32(smem + s * STAGE);
                     const uint32_t a_tmem = tmem + (uint32_t)(BN + 32 * s);
@@ -754,6 +773,7 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
             for (int kb = 0, k0 = 0; kb < nkb; ++kb, k0 += BK, ++i, (++s == NS) ? (s = 0, ph ^= 1) : 0) {
                 while ((ch_lo + 1) * KK <= k0) ++ch_lo;
                 mbar_wait(&pfull[s], (uint32_t)ph);
+                if (gt == 0) pstamp(1, i);
                 const uint8_t *patch = smem + s * STAGE + B_BYTES;
                 uint32_t v[16];
                 const int4 *trow = reinterpret_cast<const int4 *>(ktab + (k0 - ch_lo * KK) * BK + (BK / 2) * h);
@@ -781,38 +801,81 @@ kmtc_persist_kernel(const __grid_constant__ CUtensorMap tmapF, const __grid_cons
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[s]);
+                if (gt == 0) pstamp(2, i);
             }
         }
     } else {
         // ------------------------------------------------ epilogue (warps 11..14)
+        // The tile's valid pixels form ONE contiguous compact range
+        // [q0, q0 + nv) of every O plane (wide pixels run row after row).
+        // Per 32-filter chunk: TMEM -> registers -> smem [filter][pixel], then
+        // each warp writes 8 filters' runs with lanes along the run.  (Direct
+        // stores from the TMEM layout wrote 32-pixel pieces of 32 planes that
+        // start mid-line: the drain took ~15 K clk per tile while the MMA
+        // waited on tmem_empty — profiles/tc_persist_stamps_r02.txt.)
+        // kTpEpiGroups groups of four warps (one per TMEM lane quarter) take
+        // interleaved 16-column chunks, each through its own staging buffer
+        // (direct stores -> 1 -> 2 -> 4 groups: the MMA issuer waited 15 K ->
+        // 9.3 K -> 8.2 K -> 7.2 K clk at each tile boundary; 2 groups measured
+        // fastest overall, profiles/tc_persist_stamps_r02.txt).
         const int q = (int)(warp & 3);                   // TMEM lane quarter
         const int row = q * 32 + (int)lane;
+        const int eg = (int)(warp - kTpEpiWarp) >> 2;    // epilogue group
+        float *ep = reinterpret_cast<float *>(smem + NS * STAGE + 512 + geo.tab_bytes) + eg * 16 * kTcBM;
         int nt = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
             int p0, n0, img;
             tile_of(t, &p0, &n0, &img);
-            const int pe = p0 + row;
-            const int y = pe / Wx, x = pe - y * Wx;
-            const bool valid = (pe < Ho * Wx) && (x < Wo);
-            float *Oi = O + (int64_t)img * M * plane + (int64_t)y * Wo + x;
+            const int pend = min(p0 + kTcBM, Ho * Wx);
+            int y0 = p0 / Wx, x0 = p0 - y0 * Wx;
+            if (x0 >= Wo) { x0 = 0; ++y0; }              // first valid wide pixel: (y0, x0)
+            const int q0 = y0 * Wo + x0;
+            int nv = 0;
+            if (y0 * Wx + x0 < pend) {
+                const int yl = (pend - 1) / Wx, xl = pend - 1 - yl * Wx;
+                nv = yl * Wo + min(xl, Wo - 1) - q0 + 1;
+            }
+            // wide offsets (from p0) of this lane's compact elements k = lane + 32 i
+            int woff[kTcBM / 32];
+#pragma unroll
+            for (int i = 0; i < kTcBM / 32; ++i) {
+                const int k = (int)lane + 32 * i;
+                const int yy = (x0 + k) / Wo, xx = x0 + k - yy * Wo;
+                woff[i] = k < nv ? (y0 + yy) * Wx + xx - p0 : -1;
+            }
+            float *Ot = O + (int64_t)img * M * plane + q0 + lane;
             mbar_wait(tmem_full, (uint32_t)(nt & 1));
             tc_fence_after();
 #pragma unroll 1
-            for (int cb = 0; cb < BN / 32; ++cb) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32), r);
+            for (int cb = eg; cb < BN / 16; cb += kTpEpiGroups) {
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 16), r);
                 tmem_ld_wait();
-                if (valid) {
+                if (cb + kTpEpiGroups >= BN / 16) {      // this warp's last TMEM read of the tile
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tmem_empty);
+                }
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int m = n0 + cb * 32 + j;
-                        if (m < M) Oi[(int64_t)m * plane] = __uint_as_float(r[j]);
+                for (int j = 0; j < 16; ++j) ep[j * kTcBM + row] = __uint_as_float(r[j]);
+                asm volatile("bar.sync %0, 128;" ::"r"(2 + eg) : "memory");   // this group's 4 warps
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int j = q * 4 + jj;
+                    const int m = n0 + cb * 16 + j;
+                    if (m < M) {
+                        float *Om = Ot + (int64_t)m * plane;
+#pragma unroll
+                        for (int i = 0; i < kTcBM / 32; ++i)
+                            if (woff[i] >= 0) Om[32 * i] = ep[j * kTcBM + woff[i]];
                     }
                 }
+                asm volatile("bar.sync %0, 128;" ::"r"(2 + eg) : "memory");
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tmem_empty);      // TMEM free for the next tile's MMAs
+            if (eg >= BN / 16) {                         // no chunk for this group (BN < 16 * groups)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tmem_empty);
+            }
         }
     }
     __syncthreads();
@@ -891,8 +954,10 @@ static int plan_tc(int C, int Wx, int Wy, int K, int M, bool bf16, const void *F
     // one 2-D patch box per k-block, whole k-blocks; B200CONV_TC_PERSIST=0 disables
     const bool persist_on = allow_persist && env_override("B200CONV_TC_PERSIST", 1) != 0;
     if (persist_on && S == 1 && aligned && patch && tiles > num_sms() && gp.nbox == 1 &&
-        ((int64_t)Wx * Wy * elem) % 16 == 0 && Ktot % BK == 0 && gp.tab_bytes > 0) {
+        ((int64_t)Wx * Wy * elem) % 16 == 0 && Ktot % BK == 0 && gp.tab_bytes > 0 &&
+        tc_geom(Wx, K, BN, elem, true, kTpEpiBytes).stages >= 2) {
         p->tma_f |= 32;                                    // bit 5: persistent CTAs
+        p->smem_bytes = tc_geom(Wx, K, BN, elem, true, kTpEpiBytes).smem;
         p->grid_x = 1;
         p->grid_y = num_sms();
         p->grid_z = 1;

@@ -595,7 +595,7 @@ def test_simt_batched_every_tile(conv, monkeypatch, tile, split, ws):
 # epilogue of one overlapping the next one's loads); integer inputs: equal to
 # the one-tile-per-CTA kernel and to the oracle
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
-@pytest.mark.parametrize("M", [300, 200, 64])          # filter tiles of 256 (ragged), 128 (ragged), 64
+@pytest.mark.parametrize("M", [300, 200, 64, 32])      # filter tiles of 256 (ragged), 128 (ragged), 64, 32
 def test_tc_persistent_many_tiles(conv, monkeypatch, prec, M):
     dt = torch.bfloat16 if prec == "bf16" else torch.float32
     N, C, W, K = 40, 64, 28, 3                           # 40 x 6 pixel tiles (x filter tiles) > 148
