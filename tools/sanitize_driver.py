@@ -64,6 +64,12 @@ for W, K, M in [(32, 3, 4), (20, 1, 8), (40, 3, 16), (17, 5, 8), (30, 7, 4), (9,
 I, F = t(synth.uniform01(1, (21, 21))), t(synth.uniform_pm1(2, (6, 3, 3)))
 check("KS padded p1", conv.single_padded(I, F, 1)[None], I[None, None].float(), F[:, None], 1)
 check("KS strided s2 p1", conv.single_strided(I, F, 2, 1)[None], I[None, None], F[:, None], 1, 2)
+# KS-L (line-aligned flat chunks), forced on small maps of several alignment periods
+os.environ["B200CONV_KS_FLAT"] = "1"
+for W, H, M in [(30, 30, 12), (12, 9, 7), (58, 20, 20)]:
+    I, F = t(synth.uniform01(1, (H, W))), t(synth.uniform_pm1(2, (M, 3, 3)))
+    check(f"KS-L W{W}x{H} M{M}", conv.single(I, F)[None], I[None, None], F[:, None])
+os.environ.pop("B200CONV_KS_FLAT")
 # KS-C3 stems
 for prec in ("fp32", "tf32", "bf16"):
     multi(3, 40, 3, 16, prec, name="KS-C3")
@@ -82,6 +88,7 @@ for prec in ("tf32", "bf16"):
     multi(64, 14, 3, 96, prec, {"B200CONV_GM": "0", "B200CONV_TC_SPLIT": "3", "B200CONV_TC_DSMEM": "1"},
           name="KM-TC split DSMEM")
     multi(64, 28, 3, 64, prec, N=40, name="KM-TC persistent batch")
+    multi(32, 28, 3, 256, prec, N=26, name="KM-TC persistent batch BN=256")
     multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2"}, name="KM-TC/G")
     multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3"}, name="KM-TC/G split")
     multi(64, 7, 3, 256, prec, {"B200CONV_GM": "2", "B200CONV_GM_SPLIT": "3", "B200CONV_GM_DSMEM": "1"},
