@@ -137,7 +137,8 @@ def test_batched_plans():
         p32 = conv.plan_multi_batched(32, 256, 28, 28, 3, 256, prec)
         assert p32["kernel"] == 2 and p32["launches"] == 1
         if p32["tma_f"] & 32:            # persistent CTAs: one per SM walks the 32 x 6 tiles
-            assert p32["grid_y"] == 148 and p32["block_x"] == 480
+            # 8 gather + 2 producer + 1 MMA warps, two epilogue groups of 4 warps
+            assert p32["grid_y"] == 148 and p32["block_x"] == 32 * (11 + 8)
         else:
             assert p32["grid_y"] == 32 * (-(-26 * 28 // 128))
         assert p32["cluster_x"] == 1 and p1["kernel"] in (2, 3)
