@@ -379,8 +379,10 @@ ks_kernel(const KsArgs a) {
 // m, m + P, m + 2P, m + 3P, where P is the alignment period of the planes
 // (P * Ho * Wo == 0 mod 32 floats): they share the line offset h of their
 // planes, so one pixel mapping is aligned for all four.  Rows of the pair
-// never split (Wo even, p even).  The CTA owns a contiguous chunk range of one
-// filter group and stages the input rows those chunks need.
+// never split (Wo even, p even).  Units (group, chunk) are dealt evenly over
+// one wave of 3 CTAs per SM (equal work per SM: 11.9-12.2 vs 12.9 us with
+// CTAs owning chunk ranges of one group, which left SMs with 2 or 3 CTAs);
+// each CTA stages the input rows of its (at most two) groups' chunk ranges.
 struct KfArgs {
     const float *I;
     const float *F;
@@ -389,57 +391,74 @@ struct KfArgs {
     int P;        // plane alignment period (filters)
     int NG;       // filter groups: ceil(M / (4P)) * P
     int nch;      // 64-float chunks per plane (incl. the partial head chunk)
-    int nsplit;   // CTAs per filter group (contiguous chunk ranges)
+    int ub, ur;   // units U = NG * nch (u = g * nch + c) dealt to warps: [w*ub + min(w, ur), ...)
 };
+
+#ifndef B200CONV_KSL_ALIGN
+#define B200CONV_KSL_ALIGN 4
+#endif
+constexpr int kKslAlign = B200CONV_KSL_ALIGN;   // staged block B alignment (floats, power of 2)
+
+// first line-aligned flat index h of the planes of filter group g
+__device__ __forceinline__ int ksl_h(int g, int P, int64_t plane) {
+    return (32 - (int)(((int64_t)(g % P) * (plane & 31)) & 31)) & 31;
+}
+
+// Input rows [row_lo, row_hi) of chunks [c0, c1) of a group with head h.
+__device__ __forceinline__ void ksl_rows(int h, int c0, int c1, int HW, int Wo, int Wy, int *lo, int *hi) {
+    const int p_lo = max(0, h + 64 * (c0 - 1)), p_hi = min(HW - 1, h + 64 * c1 - 1);
+    *lo = p_lo / Wo;
+    *hi = max(*lo, min(Wy, p_hi / Wo + 3));
+}
 
 __global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) {
     constexpr int K = 3, R = 4;
     extern __shared__ __align__(16) float smem[];
-    const int Wx = a.Wx, Wy = a.Wy, M = a.M, P = a.P;
+    const int Wx = a.Wx, Wy = a.Wy, M = a.M, P = a.P, nch = a.nch;
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
     const int HW = Ho * Wo;
     const int64_t plane = HW;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // CTA -> (filter group, contiguous chunk range); warp -> an eighth of it.
-    // Each warp writes long contiguous ranges of its four planes.
-    const int g = blockIdx.x / a.nsplit, sp = blockIdx.x - g * a.nsplit;
-    const int cs0 = (int)((int64_t)sp * a.nch / a.nsplit), cs1 = (int)((int64_t)(sp + 1) * a.nch / a.nsplit);
-    const int wc0 = cs0 + (int)((int64_t)warp * (cs1 - cs0) / kKsWarps);
-    const int wc1 = cs0 + (int)((int64_t)(warp + 1) * (cs1 - cs0) / kKsWarps);
-    const int gb = g / P, r = g - gb * P;
-    const int h = (32 - (int)(((int64_t)r * (plane & 31)) & 31)) & 31;   // first line-aligned p of these planes
-    const int m0 = gb * P * R + r;
-    // taps of the four filters, [t][f] (FFMA2 pairs along filters)
-    float w[9 * R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        const int m = m0 + P * i;
-#pragma unroll
-        for (int t = 0; t < 9; ++t) w[t * R + i] = 0.f;
-        if (m < M) {
-#pragma unroll
-            for (int t = 0; t < 9; ++t) w[t * R + i] = __ldg(a.F + (int64_t)m * 9 + t);
-        }
+    // Units u = g * nch + c (group-major: a warp writes long contiguous runs of
+    // its group's four planes) dealt evenly over every warp of one wave of 3
+    // CTAs per SM (equal work per SM).  A CTA's range covers at most two
+    // groups (the planner checks): the end of group gA's planes and the start
+    // of group gA + 1's, each with its own staged row block.
+    const int cw = blockIdx.x * kKsWarps;
+    const int u0 = cw * a.ub + min(cw, a.ur), u1 = (cw + kKsWarps) * a.ub + min(cw + kKsWarps, a.ur);
+    if (u0 >= u1) { pdl_trigger(); return; }
+    // (small planes: a CTA spanning three or more groups stages the whole map once)
+    const int gA = u0 / nch, gB = (u1 - 1) / nch;
+    const bool whole = gB > gA + 1;
+    const int cA0 = u0 - gA * nch, cA1 = gB == gA ? u1 - gA * nch : nch;
+    const int cB1 = gB == gA ? 0 : u1 - gB * nch;
+    int rA0 = 0, rA1 = Wy, rB0 = 0, rB1 = 0;
+    if (!whole) {
+        ksl_rows(ksl_h(gA, P, plane), cA0, cA1, HW, Wo, Wy, &rA0, &rA1);
+        if (gB != gA) ksl_rows(ksl_h(gB, P, plane), 0, cB1, HW, Wo, Wy, &rB0, &rB1);
     }
-    // the CTA stages the input rows of its chunk range (measured faster than
-    // per-warp row ranges: 12.7 vs 13.2 us on 224x224 M=256)
-    const int p_lo = max(0, h + 64 * (cs0 - 1)), p_hi = min(HW - 1, h + 64 * cs1 - 1);
-    const int row_lo = p_lo / Wo, row_hi = min(Wy, p_hi / Wo + K);
-    const int64_t e0 = (int64_t)row_lo * Wx, e1 = (int64_t)row_hi * Wx;
-    const int pad = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + e0) & 3);
+    const int64_t eA = (int64_t)rA0 * Wx, eB = (int64_t)rB0 * Wx;
+    const int padA = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + eA) & 3);
+    const int padB = (int)(((reinterpret_cast<uintptr_t>(a.I) >> 2) + eB) & 3);
+    // block B follows block A's actual extent (16-B aligned)
+    float *sA = smem, *sB = smem + ((padA + (rA1 - rA0) * Wx + 3 + kKslAlign) & ~(kKslAlign - 1));
     pdl_wait();
-    {
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) {
+        const int64_t e0 = b ? eB : eA, e1 = b ? (int64_t)rB1 * Wx : (int64_t)rA1 * Wx;
+        const int pad = b ? padB : padA;
+        float *dst = b ? sB : sA;
         const int n16 = (int)((pad + (e1 - e0) + 3) >> 2);
         for (int c = tid; c < n16; c += kKsThreads) {
             const int64_t e = e0 - pad + 4 * c;
             if (e >= e0 && e + 4 <= e1) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             ::"r"(smem_u32(smem + 4 * c)), "l"(a.I + e) : "memory");
+                             ::"r"(smem_u32(dst + 4 * c)), "l"(a.I + e) : "memory");
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const bool ok = e + i >= e0 && e + i < e1;
-                    cp_async4(smem + 4 * c + i, ok ? a.I + e + i : a.I, ok);
+                    cp_async4(dst + 4 * c + i, ok ? a.I + e + i : a.I, ok);
                 }
             }
         }
@@ -448,13 +467,35 @@ __global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) 
     pdl_trigger();
     cp_async_wait<0>();
     __syncthreads();
-    if (wc0 >= wc1) return;
-    const float *sin = smem + pad - e0;                  // sin[y*Wx + x] = I[y][x]
-    float *O0 = a.O + (int64_t)m0 * plane;
-    int p = h + 64 * (wc0 - 1) + 2 * lane;
-    int y = 0, x = p;
-    if (p >= 0) { y = p / Wo; x = p - y * Wo; }
-    for (int c = wc0; c < wc1; ++c) {
+    const int gw = cw + warp;
+    const int w0 = gw * a.ub + min(gw, a.ur), w1 = (gw + 1) * a.ub + min(gw + 1, a.ur);
+    if (w0 >= w1) return;
+    int g = w0 / nch, c = w0 - g * nch;
+    float w[9 * R];
+    float *O0 = a.O;
+    const float *sin = sA;
+    int64_t e0 = eA;
+    int m0 = 0, p = 0, y = 0, x = 0;
+    bool fresh = true;
+    for (int u = w0; u < w1; ++u) {
+        if (fresh) {                                     // (warp-uniform) first unit of a group run
+            fresh = false;
+            const int gb = g / P, r = g - gb * P;
+            m0 = gb * P * R + r;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int m = m0 + P * i;
+#pragma unroll
+                for (int t = 0; t < 9; ++t) w[t * R + i] = m < M ? __ldg(a.F + (int64_t)m * 9 + t) : 0.f;
+            }
+            O0 = a.O + (int64_t)m0 * plane;
+            const bool inA = whole || g == gA;
+            sin = (inA ? sA + padA : sB + padB) - (inA ? eA : eB);   // sin[y*Wx + x] = I[y][x]
+            e0 = inA ? eA : eB;
+            p = ksl_h(g, P, plane) + 64 * (c - 1) + 2 * lane;
+            y = 0; x = p;
+            if (p >= 0) { y = p / Wo; x = p - y * Wo; }
+        }
         const bool valid = p >= 0 && p < HW;
         const float *base = sin + (valid ? (int64_t)y * Wx + x : e0);
         float acc[R][2];
@@ -480,9 +521,15 @@ __global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) 
             for (int i = 0; i < R; ++i)
                 if (m0 + P * i < M) stg_vec<2>(O0 + (int64_t)P * i * plane + p, acc[i]);
         }
-        p += 64;
-        x += 64;
-        while (x >= Wo) { x -= Wo; ++y; }
+        if (++c == nch) {
+            c = 0;
+            ++g;
+            fresh = true;
+        } else {
+            p += 64;
+            x += 64;
+            while (x >= Wo) { x -= Wo; ++y; }
+        }
     }
 }
 
@@ -663,9 +710,9 @@ static bool plan_ks_flat(const void *I, int Wx, int Wy, int K, int M, const floa
     const int64_t HW = (int64_t)Ho * Wo;
     if (Wo < 2 || Ho < 1 || Wo % 2 != 0 || Wx % 2 != 0 || !al(I, 8) || !al(O, 128)) return false;
     if (HW + 64 > ((int64_t)1 << 30) / 4) return false;
-    // measured (tools/ks_variants.py): 224x224 M=256 12.7 vs 14.0 us; ties at
-    // M = 128, slower below and on 112-114 px maps (the row-block kernel's
-    // two-row register blocks and 3 CTAs/SM matter more there)
+    // measured (tools/ks_variants.py): 224x224 M=256 11.9-12.2 vs 14.0 us,
+    // M=512 21.6 vs 28.2 us; ties at M = 128 and on 112-114 px maps, slower
+    // below (the row-block kernel's two-row register blocks matter more there)
     if (v != 1 && (Wo % 32 == 0 || Ho < 128 || M < 256)) return false;
     int gcd = 32, q = (int)(HW & 31);
     for (int b = q; b != 0;) { const int t = gcd % b; gcd = b; b = t; }
@@ -675,17 +722,20 @@ static bool plan_ks_flat(const void *I, int Wx, int Wy, int K, int M, const floa
     a.P = P;
     a.NG = (M + 4 * P - 1) / (4 * P) * P;
     a.nch = (int)(1 + (HW + 63) / 64);
-    // one wave of 3 CTAs per SM: contiguous chunk ranges per filter group
-    int ns = 3 * num_sms() / a.NG;
-    if (kDiag) ns = env_override("B200CONV_KS_FLAT_NS", ns);
-    if (ns < 1) ns = 1;
-    if (ns > a.nch) ns = a.nch;
-    a.nsplit = ns;
-    const int G = a.NG * ns;
-    // staged rows of the longest CTA range: chunks + head/tail slack, + K - 1
-    const int64_t span = (int64_t)(a.nch + ns - 1) / ns * 64 + 64 + 32;
-    const int64_t rows = span / Wo + 2 + K;
-    const int64_t sm = ((rows < Wy ? rows : Wy) * Wx + 16) * 4;
+    const int64_t U = (int64_t)a.NG * a.nch;
+    if (U > ((int64_t)1 << 30)) return false;
+    // one wave of 3 CTAs per SM, units dealt evenly over its warps
+    int G = (int)((U + kKsWarps - 1) / kKsWarps);
+    if (G > 3 * num_sms()) G = 3 * num_sms();
+    const int NW = G * kKsWarps;
+    a.ub = (int)(U / NW);
+    a.ur = (int)(U - (int64_t)a.ub * NW);
+    const int64_t upc = (int64_t)kKsWarps * (a.ub + 1);      // units of the largest CTA
+    // the two staged blocks together: the rows of at most upc chunks, each
+    // block + head / tail slack and K - 1 halo rows; a CTA that may span three
+    // or more groups (upc > nch: small planes) stages the whole map
+    const int64_t rows = upc > a.nch ? Wy : ((upc + 2) * 64 + 64) / Wo + 2 * (K + 2);
+    const int64_t sm = ((rows < 2 * Wy ? rows : 2 * Wy) * Wx + 20 + kKslAlign) * 4;
     if (sm > 72 * 1024) return false;
     *fa = a;
     *Gout = G;
