@@ -389,6 +389,7 @@ struct KfArgs {
     float *O;
     int Wx, Wy, M;
     int P;        // plane alignment period (filters)
+    int R;        // filters per lane (4, or 8 at 2 CTAs per SM)
     int NG;       // filter groups: ceil(M / (4P)) * P
     int nch;      // 64-float chunks per plane (incl. the partial head chunk)
     int ub, ur;   // units U = NG * nch (u = g * nch + c) dealt to warps: [w*ub + min(w, ur), ...)
@@ -411,8 +412,9 @@ __device__ __forceinline__ void ksl_rows(int h, int c0, int c1, int HW, int Wo, 
     *hi = max(*lo, min(Wy, p_hi / Wo + 3));
 }
 
-__global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) {
-    constexpr int K = 3, R = 4;
+template <int R, int MB>   // R filters per lane (P apart), MB CTAs per SM
+__global__ void __launch_bounds__(kKsThreads, MB) ks_flat_kernel(const KfArgs a) {
+    constexpr int K = 3;
     extern __shared__ __align__(16) float smem[];
     const int Wx = a.Wx, Wy = a.Wy, M = a.M, P = a.P, nch = a.nch;
     const int Wo = Wx - K + 1, Ho = Wy - K + 1;
@@ -510,10 +512,10 @@ __global__ void __launch_bounds__(kKsThreads, 3) ks_flat_kernel(const KfArgs a) 
             for (int cc = 0; cc < K; ++cc) {
                 const int t = rr * K + cc;
 #pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    ffma2(acc[0][v], acc[1][v], win[v + cc], w[t * R], w[t * R + 1]);
-                    ffma2(acc[2][v], acc[3][v], win[v + cc], w[t * R + 2], w[t * R + 3]);
-                }
+                for (int v = 0; v < 2; ++v)
+#pragma unroll
+                    for (int f = 0; f < R; f += 2)
+                        ffma2(acc[f][v], acc[f + 1][v], win[v + cc], w[t * R + f], w[t * R + f + 1]);
             }
         }
         if (valid) {
@@ -710,23 +712,30 @@ static bool plan_ks_flat(const void *I, int Wx, int Wy, int K, int M, const floa
     const int64_t HW = (int64_t)Ho * Wo;
     if (Wo < 2 || Ho < 1 || Wo % 2 != 0 || Wx % 2 != 0 || !al(I, 8) || !al(O, 128)) return false;
     if (HW + 64 > ((int64_t)1 << 30) / 4) return false;
-    // measured (tools/ks_variants.py): 224x224 M=256 11.9-12.2 vs 14.0 us,
-    // M=512 21.6 vs 28.2 us; ties at M = 128 and on 112-114 px maps, slower
-    // below (the row-block kernel's two-row register blocks matter more there)
-    if (v != 1 && (Wo % 32 == 0 || Ho < 128 || M < 256)) return false;
+    // measured (tools/ks_variants.py, 8 filters per lane): 224x224 M=256
+    // 11.0 vs 13.7 us, M=128 7.1 vs 7.4; slower at M <= 64 and on 56-114 px
+    // maps (the row-block kernel's two-row register blocks matter more there)
+    if (v != 1 && (Wo % 32 == 0 || Ho < 128 || M < 128)) return false;
     int gcd = 32, q = (int)(HW & 31);
     for (int b = q; b != 0;) { const int t = gcd % b; gcd = b; b = t; }
     const int P = 32 / gcd;
     KfArgs a = {};
     a.Wx = Wx; a.Wy = Wy; a.M = M;
     a.P = P;
-    a.NG = (M + 4 * P - 1) / (4 * P) * P;
+    // 8 filters per lane at 2 CTAs per SM (128 registers: 72 taps + 16
+    // accumulators) measured faster than 4 at 3 CTAs per SM: 224x224 M=256
+    // 11.1 vs 12.2 us, M=512 20.9 vs 21.8, M=1024 40.8 vs 57.9 (4-filter
+    // version out of smem: row-block kernel)
+    a.R = kDiag ? env_override("B200CONV_KSL_R", 8) : 8;
+    if (a.R != 4) a.R = 8;
+    const int MB = a.R == 8 ? 2 : 3;
+    a.NG = (M + a.R * P - 1) / (a.R * P) * P;
     a.nch = (int)(1 + (HW + 63) / 64);
     const int64_t U = (int64_t)a.NG * a.nch;
     if (U > ((int64_t)1 << 30)) return false;
     // one wave of 3 CTAs per SM, units dealt evenly over its warps
     int G = (int)((U + kKsWarps - 1) / kKsWarps);
-    if (G > 3 * num_sms()) G = 3 * num_sms();
+    if (G > MB * num_sms()) G = MB * num_sms();
     const int NW = G * kKsWarps;
     a.ub = (int)(U / NW);
     a.ur = (int)(U - (int64_t)a.ub * NW);
@@ -734,9 +743,10 @@ static bool plan_ks_flat(const void *I, int Wx, int Wy, int K, int M, const floa
     // the two staged blocks together: the rows of at most upc chunks, each
     // block + head / tail slack and K - 1 halo rows; a CTA that may span three
     // or more groups (upc > nch: small planes) stages the whole map
-    const int64_t rows = upc > a.nch ? Wy : ((upc + 2) * 64 + 64) / Wo + 2 * (K + 2);
-    const int64_t sm = ((rows < 2 * Wy ? rows : 2 * Wy) * Wx + 20 + kKslAlign) * 4;
-    if (sm > 72 * 1024) return false;
+    // (upc > nch: either both blocks can be the whole map, or one whole-map block)
+    const int64_t rows = upc > a.nch ? 2 * (int64_t)Wy : ((upc + 2) * 64 + 64) / Wo + 2 * (K + 2);
+    const int64_t sm = ((rows < 2 * Wy ? rows : 2 * Wy) * Wx + 20 + 2 * kKslAlign) * 4;
+    if (sm > (MB == 3 ? 72 : 110) * 1024) return false;
     *fa = a;
     *Gout = G;
     *smem_bytes = (int)sm;
@@ -757,7 +767,7 @@ int plan_single(int Wx, int Wy, int K, int M, conv_plan *p) {
         p->grid_x = fg;
         p->grid_y = 1;
         p->grid_z = 1;
-        p->tile_m = 4;                                    // filters per lane (P apart)
+        p->tile_m = fa.R;                                 // filters per lane (P apart)
         p->tile_n = -2;                                   // marks KS-L (64-float flat chunks)
         p->smem_bytes = fsm;
         return 0;
@@ -908,7 +918,8 @@ cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K,
         int G = 0, sm = 0;
         if (plan_ks_flat(I, Wx, Wy, K, M, O, &fa, &G, &sm)) {
             fa.I = I; fa.F = F; fa.O = O;
-            if (cudaError_t e = ensure_smem((const void *)ks_flat_kernel, sm); e != cudaSuccess) return e;
+            auto kern = fa.R == 8 ? ks_flat_kernel<8, 2> : ks_flat_kernel<4, 3>;
+            if (cudaError_t e = ensure_smem((const void *)kern, sm); e != cudaSuccess) return e;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(G);
             cfg.blockDim = dim3(kKsThreads);
@@ -917,7 +928,7 @@ cudaError_t launch_single(const float *I, int Wx, int Wy, const float *F, int K,
             cudaLaunchAttribute attr[1] = {pdl_attr()};
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            return cudaLaunchKernelEx(&cfg, ks_flat_kernel, fa);
+            return cudaLaunchKernelEx(&cfg, kern, fa);
         }
     }
     KsPlan kp;

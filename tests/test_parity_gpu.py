@@ -107,7 +107,7 @@ def test_single_edge_cases(conv, Wx, Wy, K, M):
 # every plane alignment period P (1, 2, 4, 8, 16), filter counts that leave
 # groups partly empty, tiny and ragged maps
 KSL_SHAPES = [(10, 10, 4), (12, 9, 7), (34, 20, 33), (30, 30, 48), (58, 45, 20), (100, 37, 70),
-              (224, 224, 12), (66, 130, 9)]
+              (224, 224, 12), (66, 130, 9), (14, 14, 32), (16, 16, 64), (40, 200, 130)]
 
 
 @pytest.mark.parametrize("Wx,Wy,M", KSL_SHAPES)
