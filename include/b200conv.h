@@ -215,8 +215,9 @@ typedef struct {
     int grid_x, grid_y, grid_z;
     int block_x;
     int cluster_x;     /* split-K factor over channels / K-blocks (1 = none) */
-    int tile_m;        /* filters per CTA tile */
-    int tile_n;        /* (wide) output pixels per CTA tile */
+    int tile_m;        /* filters per CTA tile (KS: per task; KS-L: per lane, P planes apart) */
+    int tile_n;        /* (wide) output pixels per CTA tile (KS: rows per task; -1: the generic
+                          single-channel kernel; -2: KS-L, 64-float line-aligned flat chunks) */
     int smem_bytes;    /* dynamic shared memory per CTA */
     int tma_f;         /* bit 0: F tiles by TMA; bit 1: I patch by TMA (KM-TC); bit 2: im2col tiles by
                           TMA (KM-TC/G); bit 3: filters on the 128-lane M side (KM-TC/G); bit 5:
