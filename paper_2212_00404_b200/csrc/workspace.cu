@@ -117,6 +117,14 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
                      float *__restrict__ O, int plane, const PeerOut po) {
     pdl_wait();
     pdl_trigger();
+    // plain compact output, 16-B aligned rows: vector stores (peer / multicast
+    // destinations keep the per-element out_store).  Only with one lane per
+    // float4 (kRedG == 1): with 8-lane groups (S > 16) the vector store made
+    // the PDL-chained call 4 us slower on ResNet 14x14 (S = 32: 15.3 vs
+    // 11.4 us) although the reduce kernel alone was 4 % faster; configs[4]
+    // (S = 6): 114.4 -> 113.9 us.
+    const bool vec_ok = kRedG == 1 && !kBatch && po.mc == nullptr && po.n == 0 && (N & 3) == 0 &&
+                        (reinterpret_cast<uintptr_t>(O) & 15) == 0;
     // 32-bit indexing: M * N <= INT_MAX is an ABI precondition
     const int q_per_row = (N + 3) >> 2;
     const int total = M * q_per_row;
@@ -154,9 +162,18 @@ splitk_reduce_kernel(const float *__restrict__ W, int S, int64_t slice, int M, i
             const float v[4] = {a.x, a.y, a.z, a.w};
             if constexpr (!kBatch) {
                 const int64_t o = (int64_t)m * N + n;
+                if (vec_ok && n + 4 <= N) {
+                    // one 16-B store per thread (consecutive lanes: consecutive
+                    // float4 of the compact O rows): whole sectors per warp store
+                    // (four scalar stores strided by 16 B wrote every sector in
+                    // up to four partial pieces, configs[4]: 925 K L2 write
+                    // sectors for a 2.36 MB output)
+                    *reinterpret_cast<float4 *>(O + o) = a;
+                } else {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (n + i < N) out_store(po, O, o + i, v[i]);
+                    for (int i = 0; i < 4; ++i)
+                        if (n + i < N) out_store(po, O, o + i, v[i]);
+                }
             } else {
                 // batch of N / plane images: column n + i is pixel (n+i) % plane of image (n+i) / plane
 #pragma unroll
