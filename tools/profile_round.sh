@@ -21,7 +21,7 @@ full() {  # full <name> <kernel regex> <layer label> [reps]
   echo "full $1 rc=$?"
 }
 full simt kms_kernel sweep_14x14_c512_m4096_k3:fp32
-full tcg_tf32 gemm_kernel sweep_14x14_c512_m4096_k3:tf32
+full tc4_tf32 kmtc_kernel sweep_14x14_c512_m4096_k3:tf32   # configs[4] TF32 runs on the implicit KM-TC
 full tcg_bf16 gemm_kernel sweep_14x14_c512_m4096_k3:bf16
 full tc_tf32 kmtc_kernel target_28x28_c256_m256_k3:tf32 4
 full tc_bf16 kmtc_kernel target_28x28_c256_m256_k3:bf16 4
