@@ -687,7 +687,11 @@ bool plan_ks(const void *I, int Wx, int Wy, const void *F, int K, int M, float *
             if (smem > 200 * 1024) return false;
             kp->a = a;
             kp->RR = RR;
-            kp->VL = (kC == 1 && elem == 4 && Wx % TX == 0 && al(I, 4 * TX)) ? TX : 1;
+            // window loads: TX-wide vectors, or 8-B pairs when rows are only
+            // 8-B strided (Wx = 2 mod 4 with TX = 4: 230x230 K=7 M=256 went
+            // scalar, 40.5 vs 26.6 us on 224x224)
+            kp->VL = (kC == 1 && elem == 4 && Wx % TX == 0 && al(I, 4 * TX)) ? TX
+                     : (kC == 1 && elem == 4 && TX == 4 && Wx % 2 == 0 && al(I, 8)) ? 2 : 1;
             kp->VS = (Wo % TX == 0 && al(O, 4 * TX)) ? TX : ((TX >= 2 && Wo % 2 == 0 && al(O, 8)) ? 2 : 1);
             if (RR != ks_RR(K)) kp->VL = kp->VS = 1;    // small-map variant: scalar loads / stores
             // channel planes are staged from offset 0 of 16-B aligned regions
@@ -822,13 +826,20 @@ static cudaError_t launch_ks(const KsPlan &kp, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// VL in {TX, 1}; VS in {TX, 2, 1} (2 only when TX = 4)
+// VL in {TX, 2 (TX = 4), 1}; VS in {TX, 2, 1} (2 only when TX = 4)
 template <int K>
 static cudaError_t launch_ks_v(const KsPlan &kp, cudaStream_t s) {
     constexpr int TX = ks_TX(K);
     constexpr int V2 = TX >= 2 ? 2 : 1;
     if constexpr (ks_RR(K) != 1)
         if (kp.RR == 1) return launch_ks<K, 1, 1, 1>(kp, s);
+    if constexpr (TX == 4) {
+        if (kp.VL == 2) {
+            if (kp.VS == TX) return launch_ks<K, 2, TX>(kp, s);
+            if (kp.VS == 2) return launch_ks<K, 2, 2>(kp, s);
+            return launch_ks<K, 2, 1>(kp, s);
+        }
+    }
     if (kp.VL == TX) {
         if (kp.VS == TX) return launch_ks<K, TX, TX>(kp, s);
         if (kp.VS == 2) return launch_ks<K, TX, V2>(kp, s);

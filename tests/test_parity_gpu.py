@@ -123,6 +123,17 @@ def test_single_ksl_forced_matches_oracle(conv, monkeypatch, Wx, Wy, M):
     assert np.array_equal(run_single(conv, Ii[0], Fi[:, 0]), Oi)
 
 
+# KS with 8-B window loads (TX = 4 lanes on rows that are only 8-B strided:
+# Wx = 2 mod 4), K = 1 / 4 / 5 / 7, incl. the large-map row blocks
+@pytest.mark.parametrize("Wx,Wy,K,M", [(230, 230, 7, 4), (62, 66, 5, 8), (130, 40, 5, 3), (30, 30, 1, 8),
+                                       (226, 100, 1, 16), (54, 70, 4, 5)])
+def test_single_8b_window_loads(conv, Wx, Wy, K, M):
+    I = synth.uniform01(41, (Wy, Wx))
+    F = synth.uniform_pm1(42, (M, K, K))
+    Oo, A = oracle.conv_single(I, F)
+    assert_parity(run_single(conv, I, F), Oo, A, TAU["fp32"], f"single {Wx}x{Wy} K{K} M{M}")
+
+
 def test_single_positive_stress_and_ints(conv):
     I, F = synth.layer_inputs(1, 56, 56, 7, 32, kind="positive")
     Oo, A = oracle.conv_single(I[0], F[:, 0])
